@@ -1,0 +1,292 @@
+/*
+ * oracle.c — CPU ORACLE (test infrastructure only; see oracle.h header).
+ *
+ * Follows PAPER.md:35 (§2.1 "Clipping Pipeline") step by step, with the
+ * readings O1..O9 of DESIGN.md §"Readings".  No blocking, no
+ * fusion, no SIMD; every division is a plain integer floor division of
+ * non-negative integers; sums run in ascending index order.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ O1 --
+ * Pixel -> HSV bin (hexcone HSV, OpenCV max tie-break r > g > b).
+ *   mx = max(r,g,b), mn = min(r,g,b), d = mx - mn
+ *   hue: d == 0 -> h = 0; else
+ *        mx == r: num6 = g - b (+ 6d if negative)
+ *        mx == g: num6 = 2d + (b - r)
+ *        else   : num6 = 4d + (r - g)
+ *        h = floor(nh * num6 / (6d))           (num6 in [0, 6d))
+ *   sat: s = mx == 0 ? 0 : min(ns - 1, floor(ns * d / mx))
+ *   val: v = floor(nv * mx / 256)
+ *   bin = (h * ns + s) * nv + v
+ */
+int32_t oracle_bin(int32_t r, int32_t g, int32_t b, int32_t nh, int32_t ns, int32_t nv) {
+  int32_t mx = r;
+  if (g > mx) mx = g;
+  if (b > mx) mx = b;
+  int32_t mn = r;
+  if (g < mn) mn = g;
+  if (b < mn) mn = b;
+  int32_t d = mx - mn;
+
+  int32_t h;
+  if (d == 0) {
+    h = 0;
+  } else {
+    int32_t num6;
+    if (mx == r) {
+      num6 = g - b;
+      if (num6 < 0) num6 += 6 * d;
+    } else if (mx == g) {
+      num6 = 2 * d + (b - r);
+    } else {
+      num6 = 4 * d + (r - g);
+    }
+    h = (nh * num6) / (6 * d);
+  }
+
+  int32_t s;
+  if (mx == 0) {
+    s = 0;
+  } else {
+    s = (ns * d) / mx;
+    if (s > ns - 1) s = ns - 1;
+  }
+
+  int32_t v = (nv * mx) / 256;
+
+  return (h * ns + s) * nv + v;
+}
+
+void oracle_bin_table(int32_t nh, int32_t ns, int32_t nv, uint8_t* table) {
+  for (int32_t r = 0; r < 256; ++r)
+    for (int32_t g = 0; g < 256; ++g)
+      for (int32_t b = 0; b < 256; ++b)
+        table[(r << 16) | (g << 8) | b] = (uint8_t)oracle_bin(r, g, b, nh, ns, nv);
+}
+
+/* ------------------------------------------------------------------ O2 --
+ * hist_t[b] = #{pixels of frame t with bin b}; every pixel is analysed
+ * (no downscaling, cropping or letterbox handling). */
+void oracle_hist(const uint8_t* frame, int64_t npix, int32_t nh, int32_t ns, int32_t nv,
+                 uint32_t* hist) {
+  int32_t nbins = nh * ns * nv;
+  for (int32_t i = 0; i < nbins; ++i) hist[i] = 0;
+  for (int64_t p = 0; p < npix; ++p) {
+    int32_t r = frame[3 * p + 0];
+    int32_t g = frame[3 * p + 1];
+    int32_t b = frame[3 * p + 2];
+    hist[oracle_bin(r, g, b, nh, ns, nv)] += 1;
+  }
+}
+
+typedef struct {
+  const uint8_t* frames;
+  int64_t f0, f1, npix;
+  int32_t nh, ns, nv;
+  uint32_t* hist;
+} hist_job;
+
+static void* hist_worker(void* arg) {
+  hist_job* j = (hist_job*)arg;
+  int32_t nbins = j->nh * j->ns * j->nv;
+  for (int64_t f = j->f0; f < j->f1; ++f)
+    oracle_hist(j->frames + f * j->npix * 3, j->npix, j->nh, j->ns, j->nv,
+                j->hist + f * nbins);
+  return NULL;
+}
+
+void oracle_hist_frames(const uint8_t* frames, int64_t n, int64_t npix, int32_t nh, int32_t ns,
+                        int32_t nv, uint32_t* hist, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (nthreads > n) nthreads = (int)(n > 0 ? n : 1);
+  pthread_t th[256];
+  hist_job jobs[256];
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i].frames = frames;
+    jobs[i].f0 = n * i / nthreads;
+    jobs[i].f1 = n * (i + 1) / nthreads;
+    jobs[i].npix = npix;
+    jobs[i].nh = nh;
+    jobs[i].ns = ns;
+    jobs[i].nv = nv;
+    jobs[i].hist = hist;
+  }
+  if (nthreads == 1) {
+    hist_worker(&jobs[0]);
+    return;
+  }
+  for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, hist_worker, &jobs[i]);
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
+/* ------------------------------------------------------------------ O3 --
+ * L1_t = sum_b |hist_t[b] - hist_{t-1}[b]| for t >= 1, L1_0 = 0;
+ * score_t = L1_t / (2N), one IEEE f64 division (total-variation distance). */
+void oracle_l1(const uint32_t* hist, int64_t n, int32_t nbins, int64_t npix, uint32_t* l1,
+               double* score) {
+  for (int64_t t = 0; t < n; ++t) {
+    uint64_t acc = 0;
+    if (t >= 1) {
+      for (int32_t b = 0; b < nbins; ++b) {
+        int64_t a = hist[t * nbins + b];
+        int64_t c = hist[(t - 1) * nbins + b];
+        acc += (uint64_t)(a > c ? a - c : c - a);
+      }
+    }
+    l1[t] = (uint32_t)acc;
+    if (score) score[t] = (double)acc / (double)(2 * npix);
+  }
+}
+
+/* ------------------------------------------------------------------ O4 --
+ * Candidate <=> t >= 1 and L1_t * 10^6 >= tau_ppm * 2N (exact, u64). */
+int64_t oracle_candidates(const uint32_t* l1, int64_t n, int64_t npix, int64_t tau_ppm,
+                          int64_t* cand) {
+  int64_t k = 0;
+  for (int64_t t = 1; t < n; ++t) {
+    uint64_t lhs = (uint64_t)l1[t] * 1000000ull;
+    uint64_t rhs = (uint64_t)tau_ppm * (uint64_t)(2 * npix);
+    if (lhs >= rhs) cand[k++] = t;
+  }
+  return k;
+}
+
+/* ------------------------------------------------------------- O5 + O6 --
+ * O5: last = 0; for candidates t ascending: accept t iff t - last >= L_min.
+ * O6: if any cut was accepted and n - last < L_min, drop the last accepted cut. */
+int64_t oracle_min_length(const int64_t* cand, int64_t n_cand, int64_t n, int64_t l_min,
+                          int64_t* cuts) {
+  int64_t last = 0, k = 0;
+  for (int64_t i = 0; i < n_cand; ++i) {
+    int64_t t = cand[i];
+    if (t - last >= l_min) {
+      cuts[k++] = t;
+      last = t;
+    }
+  }
+  if (k > 0 && n - last < l_min) k -= 1;
+  return k;
+}
+
+/* ------------------------------------------------------------------ O8 --
+ * Clip embedding S = sum of the clip's per-frame image embeddings, f64,
+ * ascending frame order (the sum is equivalent to the mean for cosine). */
+void oracle_clip_sum(const float* emb, int64_t dim, int64_t f0, int64_t f1, double* S) {
+  for (int64_t d = 0; d < dim; ++d) S[d] = 0.0;
+  for (int64_t f = f0; f < f1; ++f)
+    for (int64_t d = 0; d < dim; ++d) S[d] += (double)emb[f * dim + d];
+}
+
+double oracle_cosine(const double* a, const double* b, int64_t dim) {
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  for (int64_t d = 0; d < dim; ++d) {
+    dot += a[d] * b[d];
+    na += a[d] * a[d];
+    nb += b[d] * b[d];
+  }
+  na = sqrt(na);
+  nb = sqrt(nb);
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  return dot / (na * nb);
+}
+
+/* ------------------------------------------------------------------ O9 --
+ * Round-synchronous merge to a fixed point:
+ *   B = [0] ++ cuts ++ [n]; repeat: c_k = cos(S_k, S_{k+1}) for every adjacent
+ *   pair; M = {k : c_k >= theta}; if M is empty stop; else remove B_{k+1} for
+ *   all k in M at once and recompute the S of the merged clips from frames.
+ *   Band hit <=> |c_k - theta| <= band_rel * theta (counted in every round). */
+int64_t oracle_merge(const float* emb, int64_t n, int64_t dim, const int64_t* cuts,
+                     int64_t n_cuts, double theta, double band_rel, int32_t max_rounds,
+                     int64_t* final_cuts, double* cos_at_decision, int64_t* n_band_hits,
+                     int32_t* rounds) {
+  /* B holds the boundaries; idx[j] = index of B[j] among the detected cuts */
+  int64_t* B = (int64_t*)malloc(sizeof(int64_t) * (n_cuts + 2));
+  int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (n_cuts + 2));
+  int64_t nb = 0;
+  B[nb] = 0;
+  idx[nb++] = -1;
+  for (int64_t j = 0; j < n_cuts; ++j) {
+    B[nb] = cuts[j];
+    idx[nb++] = j;
+  }
+  B[nb] = n;
+  idx[nb++] = -1;
+  for (int64_t j = 0; j < n_cuts; ++j) cos_at_decision[j] = 0.0;
+
+  double* S = (double*)malloc(sizeof(double) * dim * (n_cuts + 1));
+  double* c = (double*)malloc(sizeof(double) * (n_cuts + 1));
+  char* rm = (char*)malloc(n_cuts + 2);
+  int64_t hits = 0;
+  int32_t r = 0;
+  for (;;) {
+    int64_t K = nb - 1; /* clips */
+    if (K < 2) break;
+    if (max_rounds > 0 && r >= max_rounds) break;
+    for (int64_t k = 0; k < K; ++k) oracle_clip_sum(emb, dim, B[k], B[k + 1], S + k * dim);
+    int64_t m = 0;
+    for (int64_t k = 0; k + 1 < K; ++k) {
+      c[k] = oracle_cosine(S + k * dim, S + (k + 1) * dim, dim);
+      cos_at_decision[idx[k + 1]] = c[k];
+      if (fabs(c[k] - theta) <= band_rel * theta) hits += 1;
+      rm[k + 1] = (c[k] >= theta);
+      m += rm[k + 1];
+    }
+    r += 1;
+    if (m == 0) break;
+    int64_t w = 0;
+    for (int64_t j = 0; j < nb; ++j) {
+      if (j > 0 && j < nb - 1 && rm[j]) continue;
+      B[w] = B[j];
+      idx[w] = idx[j];
+      ++w;
+    }
+    nb = w;
+  }
+  int64_t nf = nb - 2;
+  for (int64_t j = 0; j < nf; ++j) final_cuts[j] = B[j + 1];
+  *n_band_hits = hits;
+  *rounds = r;
+  free(B);
+  free(idx);
+  free(S);
+  free(c);
+  free(rm);
+  return nf;
+}
+
+/* ------------------------------------------------------------ the path --
+ * O1-O2 histograms, O3 distance, O4 threshold, O5-O6 greedy + tail,
+ * O8-O9 merge on the detected cuts. */
+int oracle_video(const uint8_t* frames, int64_t n, int64_t npix, const float* emb, int64_t dim,
+                 const oracle_params* p, int nthreads, uint32_t* hist, uint32_t* l1,
+                 double* score, int64_t* detected, int64_t* final_cuts, double* cos,
+                 oracle_result* res) {
+  int32_t nbins = p->nh * p->ns * p->nv;
+  oracle_hist_frames(frames, n, npix, p->nh, p->ns, p->nv, hist, nthreads);
+  oracle_l1(hist, n, nbins, npix, l1, score);
+  int64_t* cand = (int64_t*)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+  int64_t nc = oracle_candidates(l1, n, npix, p->tau_ppm, cand);
+  int64_t nd = oracle_min_length(cand, nc, n, p->l_min, detected);
+  free(cand);
+  res->n_candidates = nc;
+  res->n_detected = nd;
+  if (emb) {
+    res->n_final = oracle_merge(emb, n, dim, detected, nd, p->theta, p->band_rel,
+                                p->max_rounds, final_cuts, cos, &res->n_band_hits,
+                                &res->rounds);
+  } else {
+    res->n_final = nd;
+    for (int64_t j = 0; j < nd; ++j) final_cuts[j] = detected[j];
+    res->n_band_hits = 0;
+    res->rounds = 0;
+  }
+  return 0;
+}

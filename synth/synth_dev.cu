@@ -1,0 +1,129 @@
+/*
+ * synth_dev.cu — device (CUDA) side of the seeded input generator (see
+ * synth.h).  Built into synth/libsynthdev.so; used by bench.py and the GPU
+ * tests to fill HBM with the same bytes the host generator produces (checked
+ * by frame hashes).  Holds no method arithmetic.
+ */
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "synth.h"
+
+namespace {
+
+constexpr int kGenThreads = 256;
+constexpr int kPxPerThread = 16;
+
+__global__ void __launch_bounds__(kGenThreads)
+gen_frames_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0,
+                  const synth_frame* __restrict__ frames, uint8_t* __restrict__ out) {
+  __shared__ uint32_t pal[8][3];
+  const int64_t f = blockIdx.y;
+  const uint32_t t = (uint32_t)(t0 + f);
+  const synth_frame fr = frames[t];
+  if (threadIdx.x < 24) {
+    uint32_t k = threadIdx.x / 3, c = threadIdx.x % 3;
+    pal[k][c] = synth_palette(seed, video, fr.scene, k, c);
+  }
+  __syncthreads();
+  const uint32_t npx = W * H;
+  const uint32_t p0 = (blockIdx.x * kGenThreads + threadIdx.x) * kPxPerThread;
+  if (p0 >= npx) return;  // npx is a multiple of 16
+  const uint32_t key = synth_noise_key(seed, video, t);
+  const uint32_t cell = synth_cell(W);
+  uint32_t bytes[12];
+  uint8_t* b8 = reinterpret_cast<uint8_t*>(bytes);
+  uint32_t x = p0 % W, y = p0 / W;
+  uint32_t memo_cx = 0xFFFFFFFFu, memo_cy = 0xFFFFFFFFu, memo_k = 0;
+#pragma unroll 4
+  for (int i = 0; i < kPxPerThread; ++i) {
+    uint32_t cx = x / cell + t / 8u, cy = y / cell;
+    if (cx != memo_cx || cy != memo_cy) {
+      memo_k = synth_cell_index(seed, video, fr.scene, cx, cy);
+      memo_cx = cx;
+      memo_cy = cy;
+    }
+    uint32_t word = synth_noise_word(key, p0 + i);
+    synth_finish_pixel(pal[memo_k][0], pal[memo_k][1], pal[memo_k][2], word, fr.mode, fr.fade_w,
+                       b8 + 3 * i);
+    if (++x == W) {
+      x = 0;
+      ++y;
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)f * npx * 3 + (size_t)p0 * 3);
+  dst[0] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
+  dst[1] = make_uint4(bytes[4], bytes[5], bytes[6], bytes[7]);
+  dst[2] = make_uint4(bytes[8], bytes[9], bytes[10], bytes[11]);
+}
+
+__global__ void gen_emb_kernel(uint64_t seed, uint32_t video, int64_t t0, uint32_t D,
+                               const synth_frame* __restrict__ frames, float* __restrict__ out) {
+  const int64_t f = blockIdx.x;
+  const uint32_t t = (uint32_t)(t0 + f);
+  const uint32_t s = frames[t].scene;
+  const uint32_t key = synth_emb_key(seed, video, t);
+  for (uint32_t d = threadIdx.x; d < D; d += blockDim.x)
+    out[(size_t)f * D + d] = synth_emb_value(synth_emb_dir(seed, video, s, d), key, d);
+}
+
+__global__ void frame_hash_kernel(const uint8_t* __restrict__ frames, int64_t bytes_per_frame,
+                                  unsigned long long* __restrict__ out) {
+  const int64_t f = blockIdx.y;
+  const int64_t nw = bytes_per_frame / 8;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(frames + f * bytes_per_frame);
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += synth_hash_word(w[i], (uint64_t)i);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out + f, acc);
+}
+
+}  // namespace
+
+extern "C" {
+
+/* Frames t0..t0+n-1 of one video into d_out ([n][H][W][3] u8, device).
+ * d_frames: device array of synth_frame indexed by absolute frame index.
+ * Returns a cudaError_t value (0 = success). */
+int synth_dev_gen_frames(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0,
+                         int64_t n, const synth_frame* d_frames, uint8_t* d_out,
+                         uintptr_t stream) {
+  if (n <= 0) return 0;
+  if ((W * H) % 16 != 0) return (int)cudaErrorInvalidValue;
+  uint32_t groups = W * H / kPxPerThread;
+  for (int64_t f0 = 0; f0 < n; f0 += 65535) {
+    int64_t nf = n - f0 < 65535 ? n - f0 : 65535;
+    dim3 grid((groups + kGenThreads - 1) / kGenThreads, (unsigned)nf);
+    gen_frames_kernel<<<grid, kGenThreads, 0, (cudaStream_t)stream>>>(
+        seed, video, W, H, t0 + f0, d_frames, d_out + (size_t)f0 * W * H * 3);
+  }
+  return (int)cudaGetLastError();
+}
+
+/* Embeddings of frames t0..t0+n-1 into d_out ([n][D] f32, device). */
+int synth_dev_gen_emb(uint64_t seed, uint32_t video, int64_t t0, int64_t n, uint32_t D,
+                      const synth_frame* d_frames, float* d_out, uintptr_t stream) {
+  if (n <= 0) return 0;
+  gen_emb_kernel<<<(unsigned)n, 256, 0, (cudaStream_t)stream>>>(seed, video, t0, D, d_frames,
+                                                                 d_out);
+  return (int)cudaGetLastError();
+}
+
+/* Frame hashes (synth.h definition) of n frames; d_out [n] u64 is zeroed here. */
+int synth_dev_frame_hash(const uint8_t* d_frames, int64_t n, int64_t bytes_per_frame,
+                         uint64_t* d_out, uintptr_t stream) {
+  if (n <= 0) return 0;
+  cudaMemsetAsync(d_out, 0, sizeof(uint64_t) * n, (cudaStream_t)stream);
+  for (int64_t f0 = 0; f0 < n; f0 += 65535) {
+    int64_t nf = n - f0 < 65535 ? n - f0 : 65535;
+    dim3 grid(16, (unsigned)nf);
+    frame_hash_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        d_frames + f0 * bytes_per_frame, bytes_per_frame,
+        reinterpret_cast<unsigned long long*>(d_out + f0));
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"
