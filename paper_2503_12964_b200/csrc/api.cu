@@ -1,0 +1,759 @@
+// api.cu — the C ABI of libclipdetect (include/clip_detect.h): validation,
+// ctx scratch management, launch bookkeeping.  All arithmetic of rows a1-a9
+// runs in the kernels of hist.cu (K1), cuts.cu (K2) and merge.cu (K3); the
+// host code here only validates, sizes grids, uploads descriptor tables and
+// copies results.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/clip_detect.h"
+#include "kernels.cuh"
+
+using namespace clipdetect;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Events {
+  cudaEvent_t e[2] = {nullptr, nullptr};
+};
+
+}  // namespace
+
+struct clip_ctx {
+  clip_params p{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  int sm_count = kSMs;
+  bool sticky = false;
+  std::string err;
+  clip_stats stats{};
+  // scratch
+  DevBuf segs, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
+      detcos, pack, pack_cos, sink;
+  DevBuf m_video, m_clip_video, m_f0, m_f1, m_piece_base, m_P, m_S, m_alive, m_alive2, m_cos_b,
+      m_cos_clip, m_counters, m_vstate, m_valive;
+  DevBuf staging[2];
+  cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+  // timing
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_spans;  // (kind, start/end)
+  // pinned host staging for small D2H
+  void* hpin = nullptr;
+  size_t hpin_bytes = 0;
+};
+
+namespace {
+
+int fail(clip_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code == CLIP_E_CUDA) c->sticky = true;
+  }
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(ctx, CLIP_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define CKS(call)                       \
+  do {                                  \
+    int s_ = (call);                    \
+    if (s_ != CLIP_OK) return s_;       \
+  } while (0)
+
+int ensure(clip_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return CLIP_OK;
+  if (b.p) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(b.p));
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  size_t want = std::max(bytes, b.bytes + b.bytes / 2);
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      b.p = nullptr;
+      return fail(ctx, CLIP_E_NOMEM, "cudaMalloc(%zu) failed", bytes);
+    }
+    want = bytes;
+  }
+  b.bytes = want;
+  return CLIP_OK;
+}
+
+template <class T>
+T* P(DevBuf& b) {
+  return reinterpret_cast<T*>(b.p);
+}
+
+int ensure_pinned(clip_ctx* ctx, size_t bytes) {
+  if (ctx->hpin_bytes >= bytes) return CLIP_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  ctx->hpin = nullptr;
+  ctx->hpin_bytes = 0;
+  size_t want = std::max(bytes, (size_t)1 << 20);
+  CK(cudaMallocHost(&ctx->hpin, want));
+  ctx->hpin_bytes = want;
+  return CLIP_OK;
+}
+
+bool timing(const clip_ctx* ctx) { return (ctx->p.flags & CLIP_FLAG_TIMING) != 0; }
+
+cudaEvent_t next_event(clip_ctx* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
+
+// kind: 0 = K1, 1 = K2, 2 = K3, 3 = whole call
+struct Span {
+  clip_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  Span(clip_ctx* c, int k) : ctx(c), kind(k) {
+    if (timing(ctx)) {
+      a = next_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  void end() {
+    if (a) {
+      cudaEvent_t b = next_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->ev_spans.push_back({kind, {a, b}});
+      a = nullptr;
+    }
+  }
+};
+
+// Called after a stream sync: fold recorded spans into the stats.
+void harvest(clip_ctx* ctx) {
+  for (auto& s : ctx->ev_spans) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s.second.first, s.second.second);
+    if (s.first == 0) ctx->stats.k1_ms += ms;
+    else if (s.first == 1) ctx->stats.k2_ms += ms;
+    else if (s.first == 2) ctx->stats.k3_ms += ms;
+    else ctx->stats.total_ms += ms;
+  }
+  ctx->ev_spans.clear();
+  ctx->ev_used = 0;
+}
+
+int check_ctx(clip_ctx* ctx) {
+  if (!ctx) return CLIP_E_INVALID;
+  if (ctx->sticky) return fail(ctx, CLIP_E_STATE, "ctx unusable after CUDA error: %s", ctx->err.c_str());
+  CK(cudaSetDevice(ctx->device));
+  return CLIP_OK;
+}
+
+uint32_t nbins_of(const clip_params& p) { return p.h_bins * p.s_bins * p.v_bins; }
+
+int k1_mode(const clip_params& p) {
+  return (p.h_bins == 18 && p.s_bins == 3 && p.v_bins == 3) ? kModeFast : kModeGeneric;
+}
+
+int64_t stages_of(int64_t groups) {
+  const int64_t sg = k1_stage_groups();
+  return (groups + sg - 1) / sg;
+}
+
+// One K1 launch over a list of segments (hist pointers already set).
+int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
+  int64_t total = 0;
+  for (auto& s : segs) {
+    s.stages = stages_of(s.groups);
+    s.stage_base = total;
+    total += s.n_frames * s.stages;
+  }
+  if (total == 0) return CLIP_OK;
+  CKS(ensure(ctx, ctx->segs, segs.size() * sizeof(HistSeg)));
+  CK(cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(HistSeg),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CKS(ensure(ctx, ctx->sink, 16));
+  const int grid = k1_grid(ctx->sm_count, total);
+  Span sp(ctx, 0);
+  CK(k1_launch(mode, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total, ctx->p.h_bins,
+               ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), grid, ctx->stream));
+  sp.end();
+  ctx->stats.k1_launches += 1;
+  ctx->stats.launches += 1;
+  for (auto& s : segs) ctx->stats.k1_bytes += s.n_frames * s.groups * 48;
+  return CLIP_OK;
+}
+
+int validate_params(clip_ctx* ctx, const clip_params* p) {
+  if (!p) return fail(ctx, CLIP_E_INVALID, "params is NULL");
+  if (p->abi_version != CLIP_ABI_VERSION)
+    return fail(ctx, CLIP_E_INVALID, "abi_version %u != %u", p->abi_version, CLIP_ABI_VERSION);
+  if (p->h_bins < 1 || p->s_bins < 1 || p->v_bins < 1 || p->v_bins > 256 ||
+      (uint64_t)p->h_bins * p->s_bins * p->v_bins > 256)
+    return fail(ctx, CLIP_E_INVALID, "bins %u x %u x %u: need >= 1 each and product <= 256",
+                p->h_bins, p->s_bins, p->v_bins);
+  if (p->min_clip_frames < 1) return fail(ctx, CLIP_E_INVALID, "min_clip_frames must be >= 1");
+  if (p->cut_threshold_ppm > 1000000) return fail(ctx, CLIP_E_INVALID, "cut_threshold_ppm > 1e6");
+  if (!(p->merge_cos_threshold >= -1.0 && p->merge_cos_threshold <= 1.0))
+    return fail(ctx, CLIP_E_INVALID, "merge_cos_threshold outside [-1, 1]");
+  if (!(p->band_rel >= 0.0)) return fail(ctx, CLIP_E_INVALID, "band_rel < 0");
+  if (p->reserved != 0) return fail(ctx, CLIP_E_INVALID, "reserved must be 0");
+  return CLIP_OK;
+}
+
+int validate_frames(clip_ctx* ctx, const void* frames, int64_t n, int32_t h, int32_t w,
+                    bool allow_null) {
+  if (n < 1) return fail(ctx, CLIP_E_INVALID, "n_frames must be >= 1 (got %lld)", (long long)n);
+  if (h < 1 || w < 1) return fail(ctx, CLIP_E_INVALID, "bad frame size %dx%d", w, h);
+  if (((int64_t)h * w) % 16 != 0)
+    return fail(ctx, CLIP_E_INVALID, "H*W = %lld is not a multiple of 16", (long long)h * w);
+  if ((int64_t)h * w > (1ll << 31)) return fail(ctx, CLIP_E_INVALID, "frame too large");
+  if (!frames && !allow_null) return fail(ctx, CLIP_E_INVALID, "frames is NULL");
+  if (frames && ((uintptr_t)frames & 15)) return fail(ctx, CLIP_E_INVALID, "frames not 16-byte aligned");
+  return CLIP_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------------ merge core
+// Runs K3 on the detected cuts (device, per video at cut_base) of nv videos.
+// Writes final cuts (same layout), n_final[v] (device) and detected cosines.
+struct MergeOut {
+  int64_t band_hits_total = 0;
+  std::vector<int64_t> vstate;  // [nv][4]
+};
+
+int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, const int32_t* d_cuts,
+              int32_t* d_final, int32_t* d_nfinal, double* d_detcos, MergeOut& mo) {
+  const int32_t nv = (int32_t)mvh.size();
+  int64_t K = 0, pieces = 0;
+  for (auto& m : mvh) {
+    K += m.n_clips;
+    pieces += (m.n + kPieceFrames - 1) / kPieceFrames;
+  }
+  pieces += K;
+  CKS(ensure(ctx, ctx->m_video, sizeof(MergeVideo) * nv));
+  CKS(ensure(ctx, ctx->m_clip_video, 4 * K));
+  CKS(ensure(ctx, ctx->m_f0, 4 * K));
+  CKS(ensure(ctx, ctx->m_f1, 4 * K));
+  CKS(ensure(ctx, ctx->m_piece_base, 4 * (K + 1)));
+  CKS(ensure(ctx, ctx->m_P, sizeof(double) * pieces * dim));
+  CKS(ensure(ctx, ctx->m_S, sizeof(double) * K * dim));
+  CKS(ensure(ctx, ctx->m_alive, 4 * K));
+  CKS(ensure(ctx, ctx->m_alive2, 4 * K));
+  CKS(ensure(ctx, ctx->m_cos_b, 8 * K));
+  CKS(ensure(ctx, ctx->m_cos_clip, 8 * K));
+  CKS(ensure(ctx, ctx->m_counters, 8 * 4));
+  CKS(ensure(ctx, ctx->m_vstate, 8 * 4 * nv));
+  CKS(ensure(ctx, ctx->m_valive, 8 * nv));
+  CKS(ensure_pinned(ctx, std::max<size_t>(64, 8 * 4 * (size_t)nv)));
+  CK(cudaMemcpyAsync(ctx->m_video.p, mvh.data(), sizeof(MergeVideo) * nv, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemsetAsync(ctx->m_cos_clip.p, 0, 8 * K, ctx->stream));
+  MergeScratch s;
+  s.clip_video = P<int32_t>(ctx->m_clip_video);
+  s.clip_f0 = P<int32_t>(ctx->m_f0);
+  s.clip_f1 = P<int32_t>(ctx->m_f1);
+  s.piece_base = P<int32_t>(ctx->m_piece_base);
+  s.P = P<double>(ctx->m_P);
+  s.S = P<double>(ctx->m_S);
+  s.alive = P<int32_t>(ctx->m_alive);
+  s.alive2 = P<int32_t>(ctx->m_alive2);
+  s.cos_b = P<double>(ctx->m_cos_b);
+  s.cos_clip = P<double>(ctx->m_cos_clip);
+  s.counters = P<int64_t>(ctx->m_counters);
+  s.vstate = P<int64_t>(ctx->m_vstate);
+  s.valive = P<int64_t>(ctx->m_valive);
+  const MergeVideo* d_mv = P<MergeVideo>(ctx->m_video);
+
+  Span sp(ctx, 2);
+  CK(k3_prepare_launch(d_mv, nv, (int32_t)K, d_cuts, s, ctx->stream));
+  CK(k3_piece_sum_launch(d_mv, nv, (int32_t)K, dim, pieces, s, ctx->stream));
+  CK(k3_clip_sum_launch((int32_t)K, dim, s, ctx->stream));
+  ctx->stats.launches += 4;
+  int64_t n_alive = K - nv;
+  uint32_t r = 0;
+  while (n_alive > 0 && (ctx->p.max_merge_rounds == 0 || r < ctx->p.max_merge_rounds)) {
+    CK(k3_round_launch(d_mv, nv, dim, n_alive, ctx->p.merge_cos_threshold, ctx->p.band_rel, s,
+                       ctx->stream));
+    ctx->stats.launches += 2;
+    CK(cudaMemcpyAsync(ctx->hpin, s.counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.memcpy_d2h += 16;
+    const int64_t* cnt = reinterpret_cast<const int64_t*>(ctx->hpin);
+    n_alive = cnt[0];
+    const int64_t merges = cnt[1];
+    std::swap(s.alive, s.alive2);
+    ++r;
+    if (merges == 0) break;
+  }
+  CK(k3_finish_launch(d_mv, nv, (int32_t)K, n_alive, s, d_final, d_nfinal, d_detcos, ctx->stream));
+  ctx->stats.launches += 1;
+  sp.end();
+  CK(cudaMemcpyAsync(ctx->hpin, s.vstate, 8 * 4 * nv, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.memcpy_d2h += 8 * 4 * nv;
+  mo.vstate.assign(reinterpret_cast<int64_t*>(ctx->hpin), reinterpret_cast<int64_t*>(ctx->hpin) + 4 * nv);
+  return CLIP_OK;
+}
+
+// pack per-video detected / final cuts and cosines into contiguous buffers
+__global__ void pack_kernel(const VideoDesc* __restrict__ vids, int32_t nvid, int64_t F,
+                            const int32_t* __restrict__ cuts, const int32_t* __restrict__ ncuts,
+                            const int32_t* __restrict__ fin, const int32_t* __restrict__ nfin,
+                            const double* __restrict__ detcos, const int64_t* __restrict__ det_off,
+                            const int64_t* __restrict__ fin_off, int32_t* __restrict__ out,
+                            double* __restrict__ out_cos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  int32_t lo = 0, hi = nvid - 1;
+  while (lo < hi) {
+    const int32_t m = (lo + hi + 1) >> 1;
+    if (vids[m].fbase <= i) lo = m; else hi = m - 1;
+  }
+  const int64_t j = i - vids[lo].fbase;
+  if (j < ncuts[lo]) {
+    out[det_off[lo] + j] = cuts[i];
+    if (out_cos) out_cos[det_off[lo] + j] = detcos ? detcos[i] : 0.0;
+  }
+  if (fin && j < nfin[lo]) out[fin_off[lo] + j] = fin[i];
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+void clip_params_default(clip_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof *p);
+  p->abi_version = CLIP_ABI_VERSION;
+  p->h_bins = 18;
+  p->s_bins = 3;
+  p->v_bins = 3;
+  p->cut_threshold_ppm = 300000;
+  p->min_clip_frames = 8;
+  p->max_merge_rounds = 0;
+  p->merge_cos_threshold = 0.90;
+  p->band_rel = 1e-5;
+  p->flags = 0;
+}
+
+int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uintptr_t cuda_stream) {
+  if (!out) return CLIP_E_INVALID;
+  *out = nullptr;
+  int st = validate_params(nullptr, p);
+  if (st) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+    cudaGetLastError();
+    return CLIP_E_INVALID;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return CLIP_E_CUDA;
+  if (!(prop.major == 10 && prop.minor == 0)) return CLIP_E_ARCH;
+  clip_ctx* ctx = new clip_ctx();
+  ctx->p = *p;
+  ctx->device = cuda_device;
+  ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  ctx->sm_count = prop.multiProcessorCount;
+  if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return CLIP_E_CUDA;
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&ctx->copied[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->consumed[i], cudaEventDisableTiming);
+  }
+  *out = ctx;
+  return CLIP_OK;
+}
+
+int clip_detect_destroy(clip_ctx* ctx) {
+  if (!ctx) return CLIP_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->segs, &ctx->vids, &ctx->hist, &ctx->l1, &ctx->cand_slots,
+                    &ctx->cand_count, &ctx->cuts, &ctx->ncuts, &ctx->ncand, &ctx->final_cuts,
+                    &ctx->nfinal, &ctx->detcos, &ctx->pack, &ctx->pack_cos, &ctx->sink,
+                    &ctx->m_video, &ctx->m_clip_video, &ctx->m_f0, &ctx->m_f1,
+                    &ctx->m_piece_base, &ctx->m_P, &ctx->m_S, &ctx->m_alive, &ctx->m_alive2,
+                    &ctx->m_cos_b, &ctx->m_cos_clip, &ctx->m_counters, &ctx->m_vstate,
+                    &ctx->m_valive, &ctx->staging[0], &ctx->staging[1]};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->copied[i]) cudaEventDestroy(ctx->copied[i]);
+    if (ctx->consumed[i]) cudaEventDestroy(ctx->consumed[i]);
+  }
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  delete ctx;
+  return CLIP_OK;
+}
+
+const char* clip_last_error(const clip_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                      int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
+                      float* score) {
+  CKS(check_ctx(ctx));
+  CKS(validate_frames(ctx, frames, n_frames, height, width, false));
+  if (!hist) return fail(ctx, CLIP_E_INVALID, "hist is NULL");
+  const uint32_t nbins = nbins_of(ctx->p);
+  const int64_t npix = (int64_t)height * width;
+  CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins * n_frames, ctx->stream));
+  std::vector<HistSeg> segs(1);
+  segs[0].frames = frames;
+  segs[0].hist = hist;
+  segs[0].n_frames = n_frames;
+  segs[0].groups = npix / 16;
+  CKS(launch_k1(ctx, segs, k1_mode(ctx->p)));
+  if (l1 || score) {
+    VideoDesc vd{0, n_frames, npix};
+    CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
+    CK(cudaMemcpyAsync(ctx->vids.p, &vd, sizeof vd, cudaMemcpyHostToDevice, ctx->stream));
+    Span sp(ctx, 1);
+    CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1, score,
+                    ctx->p.cut_threshold_ppm, nullptr, nullptr, ctx->stream));
+    sp.end();
+    ctx->stats.launches += 1;
+  }
+  return CLIP_OK;
+}
+
+int clip_cuts(clip_ctx* ctx, const uint32_t* l1, int64_t n_frames, int64_t pixels_per_frame,
+              clip_cut_state* state, int32_t* cuts, int64_t cuts_capacity, int is_final_chunk) {
+  CKS(check_ctx(ctx));
+  if (n_frames < 0) return fail(ctx, CLIP_E_INVALID, "n_frames < 0");
+  if (n_frames > 0 && !l1) return fail(ctx, CLIP_E_INVALID, "l1 is NULL");
+  if (!state) return fail(ctx, CLIP_E_INVALID, "state is NULL");
+  if (pixels_per_frame < 1) return fail(ctx, CLIP_E_INVALID, "pixels_per_frame < 1");
+  if (cuts_capacity < 0 || (cuts_capacity > 0 && !cuts))
+    return fail(ctx, CLIP_E_INVALID, "bad cuts buffer");
+  const int64_t blocks = (n_frames + kCompactFrames - 1) / kCompactFrames;
+  CKS(ensure(ctx, ctx->cand_slots, 4 * std::max<int64_t>(1, blocks) * kCompactFrames));
+  CKS(ensure(ctx, ctx->cand_count, 4 * std::max<int64_t>(1, blocks)));
+  Span sp(ctx, 1);
+  CK(k2_stream_launch(l1, n_frames, pixels_per_frame, ctx->p.cut_threshold_ppm,
+                      ctx->p.min_clip_frames, state, cuts, cuts_capacity, is_final_chunk,
+                      P<int32_t>(ctx->cand_slots), P<int32_t>(ctx->cand_count), ctx->stream));
+  sp.end();
+  ctx->stats.launches += n_frames > 0 ? 2 : 1;
+  return CLIP_OK;
+}
+
+int clip_merge(clip_ctx* ctx, const float* emb, int64_t n_frames, int32_t dim,
+               const int32_t* cuts, int64_t n_cuts, int32_t* merged, int64_t* n_merged,
+               double* boundary_cos, int64_t* n_band_hits, int32_t* rounds) {
+  CKS(check_ctx(ctx));
+  if (!emb || n_frames < 1 || dim < 1 || dim > 65536)
+    return fail(ctx, CLIP_E_INVALID, "bad embeddings (emb %p, n %lld, dim %d)", (const void*)emb,
+                (long long)n_frames, dim);
+  if (n_cuts < 0 || n_cuts >= n_frames || (n_cuts > 0 && (!cuts || !merged)))
+    return fail(ctx, CLIP_E_INVALID, "bad cuts (n_cuts %lld)", (long long)n_cuts);
+  if (!n_merged) return fail(ctx, CLIP_E_INVALID, "n_merged is NULL");
+  if (n_frames > INT32_MAX) return fail(ctx, CLIP_E_INVALID, "n_frames too large");
+  if (n_cuts == 0) {
+    *n_merged = 0;
+    if (n_band_hits) *n_band_hits = 0;
+    if (rounds) *rounds = 0;
+    return CLIP_OK;
+  }
+  std::vector<MergeVideo> mv(1);
+  mv[0].emb = emb;
+  mv[0].n = n_frames;
+  mv[0].cut_base = 0;
+  mv[0].clip_base = 0;
+  mv[0].n_clips = (int32_t)n_cuts + 1;
+  CKS(ensure(ctx, ctx->nfinal, 4));
+  MergeOut mo;
+  CKS(run_merge(ctx, mv, dim, cuts, merged, P<int32_t>(ctx->nfinal), boundary_cos, mo));
+  int32_t nf = 0;
+  CK(cudaMemcpyAsync(ctx->hpin, ctx->nfinal.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  memcpy(&nf, ctx->hpin, 4);
+  harvest(ctx);
+  *n_merged = nf;
+  if (n_band_hits) *n_band_hits = mo.vstate[2];
+  if (rounds) *rounds = (int32_t)mo.vstate[1];
+  return CLIP_OK;
+}
+
+int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, clip_fill_fn fill,
+                    void* user, int64_t chunk_frames, int32_t* cut_buf, int64_t cut_capacity,
+                    clip_video_result* results, const clip_run_outputs* out) {
+  CKS(check_ctx(ctx));
+  if (!videos || n_videos < 1) return fail(ctx, CLIP_E_INVALID, "no videos");
+  if (!results) return fail(ctx, CLIP_E_INVALID, "results is NULL");
+  if (!cut_buf && cut_capacity > 0) return fail(ctx, CLIP_E_INVALID, "cut_buf is NULL");
+  const int32_t dim = videos[0].dim;
+  const bool merge = dim > 0;
+  int64_t F = 0, need = 0;
+  std::vector<VideoDesc> vd(n_videos);
+  const int64_t L = ctx->p.min_clip_frames;
+  for (int32_t i = 0; i < n_videos; ++i) {
+    const clip_video& v = videos[i];
+    CKS(validate_frames(ctx, v.frames, v.n_frames, v.height, v.width, fill != nullptr));
+    if (v.dim != dim) return fail(ctx, CLIP_E_INVALID, "video %d: dim %d != %d", i, v.dim, dim);
+    if (merge && !v.emb) return fail(ctx, CLIP_E_INVALID, "video %d: emb is NULL", i);
+    if (dim < 0 || dim > 65536) return fail(ctx, CLIP_E_INVALID, "bad dim %d", dim);
+    vd[i].fbase = F;
+    vd[i].n = v.n_frames;
+    vd[i].npix = (int64_t)v.height * v.width;
+    F += v.n_frames;
+    need += 2 * (v.n_frames / L + 1);
+  }
+  if (F > INT32_MAX) return fail(ctx, CLIP_E_INVALID, "too many frames in one call");
+  if (cut_capacity < need)
+    return fail(ctx, CLIP_E_CAPACITY, "cut_capacity %lld < %lld", (long long)cut_capacity,
+                (long long)need);
+  const uint32_t nbins = nbins_of(ctx->p);
+  const int mode = k1_mode(ctx->p);
+  const int64_t blocks = (F + kCompactFrames - 1) / kCompactFrames;
+  uint32_t* d_hist;
+  uint32_t* d_l1;
+  if (out && out->hist) {
+    d_hist = out->hist;
+  } else {
+    CKS(ensure(ctx, ctx->hist, sizeof(uint32_t) * nbins * F));
+    d_hist = P<uint32_t>(ctx->hist);
+  }
+  if (out && out->l1) {
+    d_l1 = out->l1;
+  } else {
+    CKS(ensure(ctx, ctx->l1, sizeof(uint32_t) * F));
+    d_l1 = P<uint32_t>(ctx->l1);
+  }
+  CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc) * n_videos));
+  CKS(ensure(ctx, ctx->cand_slots, 4 * blocks * kCompactFrames));
+  CKS(ensure(ctx, ctx->cand_count, 4 * blocks));
+  CKS(ensure(ctx, ctx->cuts, 4 * F));
+  CKS(ensure(ctx, ctx->ncuts, 4 * n_videos));
+  CKS(ensure(ctx, ctx->ncand, 4 * n_videos));
+  CKS(ensure(ctx, ctx->final_cuts, 4 * F));
+  CKS(ensure(ctx, ctx->nfinal, 4 * n_videos));
+  CKS(ensure(ctx, ctx->detcos, 8 * F));
+  CKS(ensure_pinned(ctx, 16 * (size_t)n_videos + 64));
+
+  Span whole(ctx, 3);
+  CK(cudaMemcpyAsync(ctx->vids.p, vd.data(), sizeof(VideoDesc) * n_videos, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * nbins * F, ctx->stream));
+
+  // ---- K1: device-resident videos in one launch
+  std::vector<HistSeg> segs;
+  std::vector<int32_t> streamed;
+  for (int32_t i = 0; i < n_videos; ++i) {
+    const clip_video& v = videos[i];
+    if (v.frames && is_device_ptr(v.frames)) {
+      HistSeg s{};
+      s.frames = v.frames;
+      s.hist = d_hist + vd[i].fbase * nbins;
+      s.n_frames = v.n_frames;
+      s.groups = vd[i].npix / 16;
+      segs.push_back(s);
+    } else {
+      streamed.push_back(i);
+    }
+  }
+  CKS(launch_k1(ctx, segs, mode));
+
+  // ---- K1: host / callback videos, chunk by chunk through two staging buffers
+  if (!streamed.empty()) {
+    int64_t max_fb = 0;
+    for (int32_t i : streamed) max_fb = std::max<int64_t>(max_fb, 3 * vd[i].npix);
+    int64_t cf = chunk_frames > 0 ? chunk_frames : std::max<int64_t>(1, ((int64_t)1 << 30) / max_fb);
+    CKS(ensure(ctx, ctx->staging[0], cf * max_fb));
+    CKS(ensure(ctx, ctx->staging[1], cf * max_fb));
+    int chunk_i = 0;
+    for (int32_t i : streamed) {
+      const clip_video& v = videos[i];
+      const int64_t fb = 3 * vd[i].npix;
+      for (int64_t t0 = 0; t0 < v.n_frames; t0 += cf, ++chunk_i) {
+        const int64_t m = std::min(cf, v.n_frames - t0);
+        const int b = chunk_i & 1;
+        uint8_t* dst = P<uint8_t>(ctx->staging[b]);
+        if (v.frames) {
+          CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->consumed[b], 0));
+          CK(cudaMemcpyAsync(dst, v.frames + t0 * fb, m * fb, cudaMemcpyHostToDevice,
+                             ctx->copy_stream));
+          CK(cudaEventRecord(ctx->copied[b], ctx->copy_stream));
+          CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[b], 0));
+          ctx->stats.memcpy_h2d += m * fb;
+        } else {
+          if (fill(user, i, t0, m, dst, reinterpret_cast<uintptr_t>(ctx->stream)) != 0)
+            return fail(ctx, CLIP_E_INVALID, "fill callback failed (video %d, frame %lld)", i,
+                        (long long)t0);
+        }
+        std::vector<HistSeg> one(1);
+        one[0].frames = dst;
+        one[0].hist = d_hist + (vd[i].fbase + t0) * nbins;
+        one[0].n_frames = m;
+        one[0].groups = vd[i].npix / 16;
+        CKS(launch_k1(ctx, one, mode));
+        CK(cudaEventRecord(ctx->consumed[b], ctx->stream));
+      }
+    }
+  }
+
+  // ---- K2: distance, threshold, ordered compaction, greedy + tail
+  {
+    Span sp(ctx, 1);
+    CK(k2_l1_launch(d_hist, F, P<VideoDesc>(ctx->vids), n_videos, nbins, nullptr, d_l1, nullptr,
+                    ctx->p.cut_threshold_ppm, P<int32_t>(ctx->cand_slots),
+                    P<int32_t>(ctx->cand_count), ctx->stream));
+    CK(k2_greedy_launch(P<VideoDesc>(ctx->vids), n_videos, P<int32_t>(ctx->cand_slots),
+                        P<int32_t>(ctx->cand_count), L, P<int32_t>(ctx->cuts),
+                        P<int32_t>(ctx->ncuts), P<int32_t>(ctx->ncand), ctx->stream));
+    sp.end();
+    ctx->stats.launches += 2;
+  }
+  // counts -> host (sync #1)
+  CK(cudaMemcpyAsync(ctx->hpin, ctx->ncuts.p, 4 * n_videos, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(reinterpret_cast<int32_t*>(ctx->hpin) + n_videos, ctx->ncand.p, 4 * n_videos,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.memcpy_d2h += 8 * n_videos;
+  std::vector<int32_t> ncuts(reinterpret_cast<int32_t*>(ctx->hpin),
+                             reinterpret_cast<int32_t*>(ctx->hpin) + n_videos);
+  std::vector<int32_t> ncand(reinterpret_cast<int32_t*>(ctx->hpin) + n_videos,
+                             reinterpret_cast<int32_t*>(ctx->hpin) + 2 * n_videos);
+
+  // ---- K3: merge
+  MergeOut mo;
+  mo.vstate.assign(4 * n_videos, 0);
+  int32_t* d_final = P<int32_t>(ctx->final_cuts);
+  if (merge) {
+    std::vector<MergeVideo> mv(n_videos);
+    int32_t cb = 0;
+    for (int32_t i = 0; i < n_videos; ++i) {
+      mv[i].emb = videos[i].emb;
+      mv[i].n = videos[i].n_frames;
+      mv[i].cut_base = vd[i].fbase;
+      mv[i].clip_base = cb;
+      mv[i].n_clips = ncuts[i] + 1;
+      cb += ncuts[i] + 1;
+    }
+    CKS(run_merge(ctx, mv, dim, P<int32_t>(ctx->cuts), d_final, P<int32_t>(ctx->nfinal),
+                  P<double>(ctx->detcos), mo));
+  }
+
+  // ---- pack results: per video [detected | final (n_detected reserved)]
+  std::vector<int64_t> offs(2 * n_videos);
+  int64_t total = 0;
+  for (int32_t i = 0; i < n_videos; ++i) {
+    offs[i] = total;
+    offs[n_videos + i] = total + ncuts[i];
+    total += 2 * (int64_t)ncuts[i];
+  }
+  CKS(ensure(ctx, ctx->pack, 4 * std::max<int64_t>(1, total) + 16 * n_videos + 16));
+  CKS(ensure(ctx, ctx->pack_cos, 8 * std::max<int64_t>(1, total)));
+  int64_t* d_offs = reinterpret_cast<int64_t*>(P<uint8_t>(ctx->pack) + 4 * std::max<int64_t>(1, total));
+  // offsets go after the packed cuts (8-byte aligned: total*4 rounded)
+  d_offs = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(d_offs) + 7) & ~(uintptr_t)7);
+  CK(cudaMemcpyAsync(d_offs, offs.data(), 16 * n_videos, cudaMemcpyHostToDevice, ctx->stream));
+  const bool want_cos = merge && out && out->detected_cos;
+  pack_kernel<<<(unsigned)((F + 255) / 256), 256, 0, ctx->stream>>>(
+      P<VideoDesc>(ctx->vids), n_videos, F, P<int32_t>(ctx->cuts), P<int32_t>(ctx->ncuts),
+      merge ? d_final : P<int32_t>(ctx->cuts), merge ? P<int32_t>(ctx->nfinal) : P<int32_t>(ctx->ncuts),
+      want_cos ? P<double>(ctx->detcos) : nullptr, d_offs, d_offs + n_videos, P<int32_t>(ctx->pack),
+      want_cos ? P<double>(ctx->pack_cos) : nullptr);
+  CK(cudaGetLastError());
+  ctx->stats.launches += 1;
+  if (merge) {
+    CK(cudaMemcpyAsync(ctx->hpin, ctx->nfinal.p, 4 * n_videos, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (total > 0)
+    CK(cudaMemcpyAsync(cut_buf, ctx->pack.p, 4 * total, cudaMemcpyDeviceToHost, ctx->stream));
+  if (want_cos && total > 0)
+    CK(cudaMemcpyAsync(out->detected_cos, ctx->pack_cos.p, 8 * total, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  whole.end();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.memcpy_d2h += 4 * total + (merge ? 4 * n_videos : 0) + (want_cos ? 8 * total : 0);
+  for (int32_t i = 0; i < n_videos; ++i) {
+    clip_video_result& r = results[i];
+    memset(&r, 0, sizeof r);
+    r.id = videos[i].id;
+    r.n_candidates = ncand[i];
+    r.n_detected = ncuts[i];
+    r.n_final = merge ? reinterpret_cast<int32_t*>(ctx->hpin)[i] : ncuts[i];
+    r.n_band_hits = mo.vstate[4 * i + 2];
+    r.rounds = (int32_t)mo.vstate[4 * i + 1];
+    r.detected_offset = offs[i];
+    r.final_offset = offs[n_videos + i];
+  }
+  harvest(ctx);
+  return CLIP_OK;
+}
+
+int clip_get_stats(clip_ctx* ctx, clip_stats* out, int reset) {
+  if (!ctx || !out) return CLIP_E_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  harvest(ctx);
+  *out = ctx->stats;
+  if (reset) memset(&ctx->stats, 0, sizeof ctx->stats);
+  return CLIP_OK;
+}
+
+int clip_debug_binmap(clip_ctx* ctx, uint8_t* table) {
+  CKS(check_ctx(ctx));
+  if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
+  CK(k5_binmap_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
+                      k1_mode(ctx->p) == kModeFast, ctx->stream));
+  ctx->stats.launches += 1;
+  return CLIP_OK;
+}
+
+int clip_debug_read_roofline(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames,
+                             int32_t height, int32_t width) {
+  CKS(check_ctx(ctx));
+  CKS(validate_frames(ctx, frames, n_frames, height, width, false));
+  std::vector<HistSeg> segs(1);
+  segs[0].frames = frames;
+  segs[0].hist = nullptr;
+  segs[0].n_frames = n_frames;
+  segs[0].groups = (int64_t)height * width / 16;
+  return launch_k1(ctx, segs, kModeRead);
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// kernels.cuh — host-side launchers of the libclipdetect kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace clipdetect {
+
+enum { kModeFast = 0, kModeGeneric = 1, kModeRead = 2 };
+
+// ---- K1 (hist.cu)
+size_t k1_smem_bytes();
+int k1_stage_groups();
+cudaError_t k1_configure();
+int k1_grid(int sm_count, int64_t total_stages);
+cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
+                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
+                      cudaStream_t stream);
+cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
+                             cudaStream_t stream);
+
+// ---- K2 (cuts.cu)
+struct VideoDesc {
+  int64_t fbase;  // first frame in the batch's flat frame space
+  int64_t n;      // frames
+  int64_t npix;   // H*W
+};
+constexpr int kCompactFrames = 128;  // frames per compaction block
+
+// l1/score for frames [0, F) of the flat frame space (+ optional candidate
+// flags compacted in order per 128-frame block).
+cudaError_t k2_l1_launch(const uint32_t* hist, int64_t F, const VideoDesc* d_vids, int32_t nvid,
+                         uint32_t nbins, const uint32_t* prev_hist, uint32_t* l1, float* score,
+                         uint64_t tau_ppm, int32_t* cand_slots, int32_t* cand_count,
+                         cudaStream_t stream);
+// greedy min-length + tail per video (one warp per video) over the compacted candidates.
+cudaError_t k2_greedy_launch(const VideoDesc* d_vids, int32_t nvid, const int32_t* cand_slots,
+                             const int32_t* cand_count, int64_t l_min, int32_t* cuts,
+                             int32_t* n_cuts, int32_t* n_cand, cudaStream_t stream);
+// streaming clip_cuts: compaction of one l1 chunk + stateful greedy.
+cudaError_t k2_stream_launch(const uint32_t* l1, int64_t n, int64_t npix, uint64_t tau_ppm,
+                             int64_t l_min, void* state, int32_t* cuts, int64_t cap,
+                             int is_final, int32_t* cand_slots, int32_t* cand_count,
+                             cudaStream_t stream);
+
+// ---- K3 (merge.cu)
+struct MergeVideo {
+  const float* emb;    // device [n][dim]
+  int64_t n;           // frames
+  int64_t cut_base;    // offset of this video's detected cuts in the cuts array
+  int32_t clip_base;   // first global clip index
+  int32_t n_clips;     // n_cuts + 1
+};
+constexpr int kPieceFrames = 256;
+
+struct MergeScratch {
+  int32_t* clip_video;  // [K]
+  int32_t* clip_f0;     // [K]
+  int32_t* clip_f1;     // [K]
+  int32_t* piece_base;  // [K+1]
+  double* P;            // [pieces][dim]
+  double* S;            // [K][dim]
+  int32_t* alive;       // [K]  right-clip index of each alive boundary
+  int32_t* alive2;      // [K]
+  double* cos_b;        // [K]  per alive boundary
+  double* cos_clip;     // [K]  per right-clip: cosine at its last evaluation
+  int64_t* counters;    // [4]  n_alive, merges this round, -, -
+  int64_t* vstate;      // [nv][4] done, rounds, band hits, merges this round (+ alive via vstate2)
+  int64_t* valive;      // [nv] alive boundaries of the video after the round
+};
+
+cudaError_t k3_prepare_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, const int32_t* cuts,
+                              MergeScratch s, cudaStream_t stream);
+cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim,
+                                int64_t pieces_bound, MergeScratch s, cudaStream_t stream);
+cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStream_t stream);
+// one merge round: cosines of the alive boundaries, decisions, ordered
+// compaction alive -> alive2 (the caller swaps the two pointers afterwards).
+cudaError_t k3_round_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t n_alive,
+                            double theta, double band_rel, MergeScratch s, cudaStream_t stream);
+// final cuts per video at cuts-array layout (offset cut_base, count n_final[v])
+// and the per-detected-cut cosines (same layout), from the alive list.
+cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int64_t n_alive,
+                             MergeScratch s, int32_t* final_cuts, int32_t* n_final,
+                             double* detected_cos, cudaStream_t stream);
+
+}  // namespace clipdetect

@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact: bin map, histograms, L1, candidates, detected and final cuts.
+Floating point: score is one f64 division rounded to f32 on both sides (exact);
+cosines within 1e-5 relative (BASELINE.json north_star), and every decision
+taken within that band is reported (band hits) rather than hidden.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from synth import manifest, torch_dev  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+COS_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    synth.build(device=True)
+    return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def ctx(dev):
+    from paper_2503_12964_b200 import Ctx
+    c = Ctx(device=0)
+    yield c
+    c.close()
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _dev_video(v, dev, emb=True):
+    table = torch_dev.frame_table(v, dev)
+    frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+    torch_dev.gen_frames(v, table, frames)
+    e = None
+    if emb:
+        e = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+        torch_dev.gen_emb(v, table, e)
+    return frames, e
+
+
+# ------------------------------------------------------------------ a1-a2
+def test_binmap_all_colours_fast(ctx):
+    got = ctx.debug_binmap().cpu().numpy()
+    want = oracle.bin_table()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} colours differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("bins", [(12, 4, 4), (6, 2, 2), (36, 3, 2), (8, 8, 4)])
+def test_binmap_all_colours_generic(dev, bins):
+    from paper_2503_12964_b200 import Ctx, default_params
+    c = Ctx(default_params(h_bins=bins[0], s_bins=bins[1], v_bins=bins[2]), device=0)
+    got = c.debug_binmap().cpu().numpy()
+    want = oracle.bin_table(oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2]))
+    c.close()
+    assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ a3-a4
+def _check_scores(ctx, frames_dev, frames_host, p=oracle.Params()):
+    hist, l1, score = ctx.frame_scores(frames_dev)
+    ref_h = oracle.hist_frames(frames_host, p)
+    ref_l1, ref_sc = oracle.l1(ref_h, frames_host[0].size // 3)
+    assert np.array_equal(_u32(hist), ref_h)
+    assert np.array_equal(_u32(l1), ref_l1)
+    assert np.array_equal(score.cpu().numpy(), ref_sc.astype(np.float32))
+
+
+def test_scores_c1(ctx, dev):
+    v = manifest.c1_video()
+    frames, _ = _dev_video(v, dev, emb=False)
+    _check_scores(ctx, frames, synth.gen_frames(v))
+
+
+@pytest.mark.parametrize("W,H,n", [(854, 480, 5), (4, 4, 3), (16, 1, 40), (100, 36, 7),
+                                   (1920, 1080, 2), (320, 240, 33)])
+def test_scores_random_noise_ragged(ctx, dev, W, H, n):
+    # uniform random colours: worst case for bin spread; shapes with a ragged
+    # last stage (854x480, 1080p), tiny frames (1 group), many small frames
+    rng = np.random.default_rng(W * 7 + H + n)
+    host = rng.integers(0, 256, size=(n, H, W, 3), dtype=np.uint8)
+    _check_scores(ctx, torch.from_numpy(host).to(dev), host)
+
+
+def test_scores_flat_and_permuted(ctx, dev):
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, 256, size=(240, 320, 3), dtype=np.uint8)
+    perm = base.reshape(-1, 3)[rng.permutation(240 * 320)].reshape(240, 320, 3)
+    flat = np.zeros_like(base)
+    flat[:] = (12, 200, 77)
+    host = np.stack([base, perm, flat, flat, base])
+    hist, l1, _ = ctx.frame_scores(torch.from_numpy(host).to(dev))
+    h = _u32(hist)
+    assert np.array_equal(h[0], h[1])  # permutation invariance
+    assert _u32(l1)[1] == 0 and _u32(l1)[3] == 0
+    assert np.array_equal(h, oracle.hist_frames(host))
+
+
+def test_scores_prev_hist_chunk_carry(ctx, dev):
+    v = manifest.c1_video()
+    frames, _ = _dev_video(v, dev, emb=False)
+    full_h, full_l1, _ = ctx.frame_scores(frames)
+    for split in [1, 10, 11, 33, 63]:
+        h1, l1a, _ = ctx.frame_scores(frames[:split].contiguous())
+        h2, l1b, _ = ctx.frame_scores(frames[split:].contiguous(), prev_hist=h1[-1].contiguous())
+        assert torch.equal(torch.cat([l1a, l1b]), full_l1)
+        assert torch.equal(torch.cat([h1, h2]), full_h)
+
+
+# ------------------------------------------------------------------ a5-a6
+def _stream_cuts(ctx, dev, l1_host, npix, chunks, cap=None):
+    n = l1_host.size
+    l1 = torch.from_numpy(l1_host.view(np.int32)).to(dev)
+    state = torch.zeros(4, dtype=torch.int64, device=dev)
+    cap = cap if cap is not None else n + 1
+    cuts = torch.full((max(1, cap),), -1, dtype=torch.int32, device=dev)
+    bounds = [0] + sorted(chunks) + [n]
+    for i in range(len(bounds) - 1):
+        a, b = bounds[i], bounds[i + 1]
+        ctx.cuts(l1[a:b].contiguous() if b > a else None, npix, state, cuts, i == len(bounds) - 2)
+    st = state.cpu().numpy()
+    k = int(st[3])
+    return cuts.cpu().numpy()[:min(k, cap)], st
+
+
+def test_cuts_streaming_every_split(ctx, dev):
+    rng = np.random.default_rng(12)
+    npix = 100
+    for trial in range(6):
+        n = int(rng.integers(20, 300))
+        l1 = np.where(rng.random(n) < 0.3, rng.integers(60, 201, n), rng.integers(0, 60, n)).astype(np.uint32)
+        l1[0] = 0
+        want = oracle.min_length(oracle.candidates(l1, npix), n, 8)
+        for split in range(0, n + 1, max(1, n // 25)):
+            got, st = _stream_cuts(ctx, dev, l1, npix, [split] if 0 < split < n else [])
+            assert list(got) == list(want), (trial, split)
+            assert st[0] == n and st[2] == oracle.candidates(l1, npix).size
+
+
+def test_cuts_all_candidates_closed_form(ctx, dev):
+    for n in [1, 7, 8, 15, 16, 17, 100, 1000, 4097]:
+        l1 = np.full(n, 200, dtype=np.uint32)
+        got, _ = _stream_cuts(ctx, dev, l1, 100, [n // 3, n // 2] if n > 4 else [])
+        assert list(got) == [8 * k for k in range(1, n // 8)]
+
+
+def test_cuts_capacity_overflow_reported(ctx, dev):
+    l1 = np.full(200, 200, dtype=np.uint32)
+    got, st = _stream_cuts(ctx, dev, l1, 100, [], cap=5)
+    assert st[3] == 200 // 8 - 1 and list(got) == [8, 16, 24, 32, 40]
+
+
+# ------------------------------------------------------------------ a7-a9
+def test_merge_random_vs_oracle(ctx, dev):
+    rng = np.random.default_rng(21)
+    for trial in range(25):
+        n = int(rng.integers(10, 700))
+        dim = int(rng.choice([3, 64, 768, 1000]))
+        k = int(rng.integers(0, 20))
+        cuts = sorted(set(int(x) for x in rng.integers(1, n, size=k)))
+        centres = rng.standard_normal((3, dim))
+        B = [0] + cuts + [n]
+        e = np.zeros((n, dim), dtype=np.float32)
+        for j in range(len(B) - 1):
+            c = centres[rng.integers(0, 3)] + 0.3 * rng.standard_normal(dim)
+            e[B[j]:B[j + 1]] = (c + 0.1 * rng.standard_normal((B[j + 1] - B[j], dim))).astype(np.float32)
+        ref = oracle.merge(e, cuts)
+        m, cos, hits, rounds = ctx.merge(torch.from_numpy(e).to(dev),
+                                         torch.tensor(cuts if cuts else [0], dtype=torch.int32, device=dev),
+                                         n_cuts=len(cuts))
+        assert list(m.cpu().numpy()) == list(ref.final), trial
+        if cuts:
+            np.testing.assert_allclose(cos.cpu().numpy(), ref.cos, rtol=COS_RTOL, atol=1e-12)
+        assert hits == ref.n_band_hits and rounds == ref.rounds
+
+
+def test_merge_worked_example(ctx, dev):
+    import math
+    e = np.zeros((6, 768), dtype=np.float32)
+    for i, deg in enumerate([0, 0, 0, 0, 20, -10]):
+        e[i, 0], e[i, 1] = math.cos(math.radians(deg)), math.sin(math.radians(deg))
+    m, cos, hits, rounds = ctx.merge(torch.from_numpy(e).to(dev),
+                                     torch.tensor([4, 5], dtype=torch.int32, device=dev))
+    assert m.numel() == 0 and rounds == 2
+
+
+# ------------------------------------------------------------------ a1-a9 end to end
+def _golden(name):
+    path = os.path.join(GOLDEN, f"{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    with open(path) as f:
+        return json.load(f)
+
+
+def _check_against_golden(g, res, hist=None, l1=None):
+    assert list(res.detected) == g["detected"], g["id"]
+    assert list(res.final) == g["final"], g["id"]
+    assert res.n_candidates == g["n_candidates"]
+    if res.detected_cos is not None and g["detected"]:
+        np.testing.assert_allclose(res.detected_cos, np.array(g["cos"]), rtol=COS_RTOL, atol=1e-12)
+    if hist is not None:
+        assert hashlib.sha256(np.ascontiguousarray(hist).tobytes()).hexdigest() == g["hist_sha256"]
+    if l1 is not None:
+        assert hashlib.sha256(np.ascontiguousarray(l1).tobytes()).hexdigest() == g["l1_sha256"]
+
+
+def test_run_videos_c1_golden(ctx, dev):
+    g = _golden("C1")["videos"][0]
+    v = manifest.c1_video()
+    frames, emb = _dev_video(v, dev)
+    hist = torch.empty((v.n, 162), dtype=torch.int32, device=dev)
+    l1 = torch.empty(v.n, dtype=torch.int32, device=dev)
+    res = ctx.run_videos([{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb}],
+                         hist=hist, l1=l1, want_cos=True)[0]
+    _check_against_golden(g, res, _u32(hist), _u32(l1))
+    assert res.final.tolist() == [10, 32, 53]
+
+
+def test_run_videos_c2_full_golden(ctx, dev):
+    """C2 at full size (18,000 720p frames, 49.8 GB) in the launch configuration
+    bench.py times: every histogram, L1, cut and cosine against the oracle."""
+    g = _golden("C2")["videos"][0]
+    v = manifest.c2_video()
+    frames, emb = _dev_video(v, dev)
+    fh = torch_dev.frame_hashes(frames[[int(t) for t in g["frame_hash"]]].contiguous())
+    assert [str(int(x)) for x in fh] == list(g["frame_hash"].values())
+    hist = torch.empty((v.n, 162), dtype=torch.int32, device=dev)
+    l1 = torch.empty(v.n, dtype=torch.int32, device=dev)
+    res = ctx.run_videos([{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb}],
+                         hist=hist, l1=l1, want_cos=True)[0]
+    _check_against_golden(g, res, _u32(hist), _u32(l1))
+    assert set(v.hard) <= set(res.final.tolist())
+    del frames
+    torch.cuda.empty_cache()
+
+
+def _run_config_streamed(ctx, dev, name, max_videos=None):
+    """Frames produced chunk by chunk by the device generator through the fill
+    callback (C3/C4/C5 do not fit in HBM at once)."""
+    gold = _golden(name)
+    vids = manifest.config_videos(name)
+    if max_videos:
+        vids = vids[:max_videos]
+    tables = [torch_dev.frame_table(v, dev) for v in vids]
+    embs = []
+    for v, t in zip(vids, tables):
+        e = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+        torch_dev.gen_emb(v, t, e)
+        embs.append(e)
+    F = sum(v.n for v in vids)
+    hist = torch.empty((F, 162), dtype=torch.int32, device=dev)
+    l1 = torch.empty(F, dtype=torch.int32, device=dev)
+
+    def fill(vi, t0, n, dst, stream):
+        v = vids[vi]
+        rc = synth.dev_lib().synth_dev_gen_frames(v.seed, v.id, v.W, v.H, t0, n,
+                                                  tables[vi].data_ptr(), dst, stream)
+        return rc
+
+    res = ctx.run_videos([{"n": v.n, "H": v.H, "W": v.W, "frames": None, "emb": e, "id": v.id}
+                          for v, e in zip(vids, embs)], fill=fill, hist=hist, l1=l1, want_cos=True)
+    h, l = _u32(hist), _u32(l1)
+    off = 0
+    for v, r in zip(vids, res):
+        g = gold["videos"][v.id]
+        _check_against_golden(g, r, h[off:off + v.n], l[off:off + v.n])
+        assert set(v.hard) <= set(r.final.tolist())
+        off += v.n
+    return res
+
+
+def test_run_videos_c3_golden(ctx, dev):
+    _run_config_streamed(ctx, dev, "C3")
+
+
+def test_run_videos_c4_golden(ctx, dev):
+    _run_config_streamed(ctx, dev, "C4")
+
+
+def test_run_videos_c5_golden(ctx, dev):
+    _run_config_streamed(ctx, dev, "C5")
+
+
+def test_batch_mixed_sources_equal_single(ctx, dev):
+    """Resident, host-pointer and callback videos in one call give the same
+    per-video results as one call per video (and as the oracle)."""
+    vids = [manifest.subsample(v, 150) for v in manifest.c5_videos()[:4]]
+    items, refs = [], []
+    for i, v in enumerate(vids):
+        host = synth.gen_frames(v)
+        emb = torch.from_numpy(synth.gen_emb(v)).to(dev)
+        src = [torch.from_numpy(host).to(dev), host, None, torch.from_numpy(host).to(dev)][i]
+        items.append({"n": v.n, "H": v.H, "W": v.W, "frames": src, "emb": emb, "id": i,
+                      "_host": host})
+        refs.append(oracle.run_video(host, synth.gen_emb(v)))
+    tables = {i: torch_dev.frame_table(v, dev) for i, v in enumerate(vids)}
+
+    def fill(vi, t0, n, dst, stream):
+        v = vids[vi]
+        return synth.dev_lib().synth_dev_gen_frames(v.seed, v.id, v.W, v.H, t0, n,
+                                                    tables[vi].data_ptr(), dst, stream)
+
+    res = ctx.run_videos(items, fill=fill, chunk_frames=37, want_cos=True)
+    for r, ref in zip(res, refs):
+        assert list(r.detected) == list(ref.detected)
+        assert list(r.final) == list(ref.final)
+        np.testing.assert_allclose(r.detected_cos, ref.cos, rtol=COS_RTOL, atol=1e-12)
+
+
+def test_invalid_arguments_fail_without_side_effects(ctx, dev):
+    from paper_2503_12964_b200 import ClipError
+    bad = torch.zeros((2, 3, 5, 3), dtype=torch.uint8, device=dev)  # H*W = 15
+    with pytest.raises(ClipError) as e:
+        ctx.frame_scores(bad)
+    assert e.value.code == 1
+    with pytest.raises(ClipError):
+        ctx.run_videos([{"n": 0, "H": 4, "W": 4, "frames": None, "emb": None}])
+    # ctx still usable
+    v = manifest.c1_video()
+    frames, _ = _dev_video(v, dev, emb=False)
+    ctx.frame_scores(frames)
+    torch.cuda.synchronize()
