@@ -198,8 +198,10 @@ typedef struct {
 /* Read (SYNC) and optionally reset the ctx counters. */
 int clip_get_stats(clip_ctx* ctx, clip_stats* out, int reset);
 
-/* Test hook (K5): the device bin function over all 2^24 colours into
- * table (device u8 [1<<24], index (r<<16)|(g<<8)|b).  Async. */
+/* Test hook (K5): the device bin function of the hot path over all 2^24
+ * colours into table (device u8 [2][1<<24], index (r<<16)|(g<<8)|b):
+ * table[0] = the colour evaluated in lane 0 of the two-pixel code, table[1]
+ * = in lane 1 (identical for the generic bins).  Async. */
 int clip_debug_binmap(clip_ctx* ctx, uint8_t* table);
 
 /* Bench hook (K6): stream n_frames frames through K1's TMA pipeline without

@@ -272,9 +272,9 @@ class Ctx:
 
     def debug_binmap(self):
         import torch
-        t = torch.empty(1 << 24, dtype=torch.uint8, device=f"cuda:{self.device}")
+        t = torch.empty(2 << 24, dtype=torch.uint8, device=f"cuda:{self.device}")
         self._check(self._lib.clip_debug_binmap(self._h, _ptr(t)))
-        return t
+        return t.view(2, 1 << 24)
 
     def debug_read_roofline(self, frames):
         n, H, W, _ = frames.shape

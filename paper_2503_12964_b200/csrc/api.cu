@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -36,6 +37,7 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
+  int k1_cfg = 0;  // K1 launch configuration (CLIPDETECT_K1_CFG overrides, for tuning)
   bool sticky = false;
   std::string err;
   clip_stats stats{};
@@ -201,10 +203,11 @@ int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   CK(cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(HistSeg),
                      cudaMemcpyHostToDevice, ctx->stream));
   CKS(ensure(ctx, ctx->sink, 16));
-  const int grid = k1_grid(ctx->sm_count, total);
+  const int grid = k1_grid(ctx->k1_cfg, ctx->sm_count, total);
   Span sp(ctx, 0);
-  CK(k1_launch(mode, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total, ctx->p.h_bins,
-               ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), grid, ctx->stream));
+  CK(k1_launch(mode, ctx->k1_cfg, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total,
+               ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), grid,
+               ctx->stream));
   sp.end();
   ctx->stats.k1_launches += 1;
   ctx->stats.launches += 1;
@@ -392,6 +395,10 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
   ctx->device = cuda_device;
   ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   ctx->sm_count = prop.multiProcessorCount;
+  if (const char* e = getenv("CLIPDETECT_K1_CFG")) {
+    const int c = atoi(e);
+    if (c >= 0 && c < k1_num_cfgs()) ctx->k1_cfg = c;
+  }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;

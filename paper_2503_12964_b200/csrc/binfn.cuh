@@ -9,10 +9,23 @@
 //   num = mid - min (k even, hue rising)   or   max - mid (k odd, falling),
 // so that the exact hue numerator is num6 = k*d + num over 6d (d = max - min),
 // and for nh = 18: h = 3k + floor(3*num/d), an integer threshold count.
-// Verified bit-exact against the oracle on all 2^24 colours (K5 test).
+//
+// Hot path (18, 3, 3): TWO pixels per 32-bit register (u16x2 lanes).  Every
+// threshold test a >= b is the bit j of (a - b + 2^j) in its lane (no lane
+// borrows because |a - b| < 2^j <= 2^15), and the tests are OR-ed into a
+// per-lane 11-bit CODE (bits 5..15 of the lane).  The histogram is kept over
+// codes; codes are mapped to the 162 bins (code_to_bin) only when a frame is
+// flushed.  Verified bit-exact against the oracle on all 2^24 colours, in both
+// lanes (tests/test_binfn_host.py on the CPU, K5 on the GPU).
 #pragma once
 
 #include <stdint.h>
+
+#if defined(__CUDACC__)
+#define CD_HD __host__ __device__ __forceinline__
+#else
+#define CD_HD static inline
+#endif
 
 namespace clipdetect {
 
@@ -22,33 +35,193 @@ namespace clipdetect {
 constexpr uint32_t kSector3k = (9u << 0) | (0u << 4) | (6u << 8) | (3u << 12) | (12u << 16) |
                                (15u << 20) | (0u << 24) | (0u << 28);
 
-// Fast path, (nh, ns, nv) = (18, 3, 3): 162 bins, branch-free, no division.
-__device__ __forceinline__ uint32_t bin_18_3_3(uint32_t r, uint32_t g, uint32_t b) {
-  const uint32_t mx = __vimax3_u32(r, g, b);
-  const uint32_t mn = __vimin3_u32(r, g, b);
-  const uint32_t d = mx - mn;
-  const uint32_t mid = r + g + b - mx - mn;
-  const uint32_t idx = ((r >= g) << 2) | ((g >= b) << 1) | (r >= b);
-  const uint32_t k3 = (kSector3k >> (idx << 2)) & 15u;
-  const uint32_t num = (k3 & 1u) ? (mx - mid) : (mid - mn);
-  const uint32_t d1 = max(d, 1u);  // d = 0: grey, num = 0 -> q = 0
-  const uint32_t n3 = 3u * num;
-  const uint32_t q = (n3 >= d1) + (n3 >= 2u * d1) + (num >= d1);
-  const uint32_t mx1 = max(mx, 1u);  // mx = 0: black, s = 0
-  const uint32_t d3 = 3u * d;
-  const uint32_t s = (d3 >= mx1) + (d3 >= 2u * mx1);
-  const uint32_t v = (mx >= 86u) + (mx >= 171u);  // floor(3*mx/256)
-  return (k3 + q) * 9u + s * 3u + v;
+// ------------------------------------------------------------ SIMD primitives
+CD_HD uint32_t cd_prmt(uint32_t a, uint32_t b, uint32_t sel) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+#else
+  const uint64_t x = ((uint64_t)b << 32) | a;
+  uint32_t r = 0;
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t s = (sel >> (4 * i)) & 15u;
+    uint32_t byte = (uint32_t)(x >> (8 * (s & 7u))) & 0xFFu;
+    if (s & 8u) byte = (byte & 0x80u) ? 0xFFu : 0u;
+    r |= byte << (8 * i);
+  }
+  return r;
+#endif
+}
+
+CD_HD uint32_t cd_max3_u16x2(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  return __vimax3_u16x2(a, b, c);
+#else
+  uint32_t r = 0;
+  for (int i = 0; i < 2; ++i) {
+    uint32_t x = (a >> (16 * i)) & 0xFFFFu, y = (b >> (16 * i)) & 0xFFFFu, z = (c >> (16 * i)) & 0xFFFFu;
+    uint32_t m = x > y ? x : y;
+    m = m > z ? m : z;
+    r |= m << (16 * i);
+  }
+  return r;
+#endif
+}
+
+CD_HD uint32_t cd_min3_u16x2(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  return __vimin3_u16x2(a, b, c);
+#else
+  uint32_t r = 0;
+  for (int i = 0; i < 2; ++i) {
+    uint32_t x = (a >> (16 * i)) & 0xFFFFu, y = (b >> (16 * i)) & 0xFFFFu, z = (c >> (16 * i)) & 0xFFFFu;
+    uint32_t m = x < y ? x : y;
+    m = m < z ? m : z;
+    r |= m << (16 * i);
+  }
+  return r;
+#endif
+}
+
+CD_HD uint32_t cd_max_u16x2(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  return __vmaxu2(a, b);
+#else
+  return cd_max3_u16x2(a, b, b);
+#endif
+}
+
+// ------------------------------------------------------------ code layout
+// Per 16-bit lane (one pixel):
+//   bit 5  A  = [r >= g]                 bit 11 q2 = [3num >= 2 d1]
+//   bit 6-7 v = floor(3 max / 256)       bit 12 s1 = [3d >= mx1]
+//   bit 8  q3 = [num >= d1]              bit 13 s2 = [3d >= 2 mx1]
+//   bit 9  B  = [g >= b]                 bit 14 0
+//   bit 10 q1 = [3num >= d1]             bit 15 ris = rising sector (k even)
+// d1 = max(d, 1), mx1 = max(max, 1).  Index into the code histogram: lane >> 5.
+constexpr int kCodeShift = 5;
+constexpr int kCodes = 1 << (16 - kCodeShift);  // 2048
+
+// Runtime multiplier constants.  Passed in as kernel arguments so that ptxas
+// cannot fold them and must issue IMAD / IMAD.HI: that arithmetic then runs on
+// the FMA pipe and leaves the ALU pipe (LOP3/PRMT/VIMNMX/SHF, the binding
+// pipe on sm_100) to the bit work.
+struct MadK {
+  uint32_t one, neg1, neg2, three;
+  uint32_t sh24;   // 2^24: mulhi(x, sh24) = x >> 8
+  uint32_t v3;     // 3 * 2^30: mulhi(x, v3) = (3x) >> 2
+  uint32_t sh13;   // 2^13: mulhi(x, sh13) = x >> 19
+  uint32_t sl16;   // 2^16: x * sl16 = x << 16
+};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
+
+CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+#else
+  return a * b + c;
+#endif
+}
+
+CD_HD uint32_t cd_mulhi(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+// Two pixels: R, G, B hold (channel of pixel 0) | (channel of pixel 1) << 16.
+// Every lane result below stays in [0, 2^16): no borrow or carry crosses lanes.
+CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B, MadK k) {
+  constexpr uint32_t kB15 = 0x80008000u;
+  const uint32_t mx = cd_max3_u16x2(R, G, B);
+  const uint32_t mn = cd_min3_u16x2(R, G, B);
+  const uint32_t d = cd_mad(mn, k.neg1, mx);
+  const uint32_t mid = R + G + B - mx - mn;     // two IADD3 (ALU)
+  const uint32_t na = cd_mad(mn, k.neg1, mid);  // rising numerator  mid - min
+  const uint32_t nb = cd_mad(mid, k.neg1, mx);  // falling numerator max - mid
+  const uint32_t R15 = cd_mad(R, k.one, kB15);
+  const uint32_t tA = cd_mad(G, k.neg1, R15);                     // bit 15: r >= g
+  const uint32_t tB = cd_mad(B, k.neg1, cd_mad(G, k.one, kB15));  // bit 15: g >= b
+  const uint32_t tC = cd_mad(B, k.neg1, R15);                     // bit 15: r >= b
+  const uint32_t ris = tA ^ tB ^ tC;              // bit 15: odd #(>=) <=> rising sector
+  const uint32_t pm = cd_prmt(ris, 0u, 0xBB99u);  // lane mask 0xFFFF if rising
+  const uint32_t num = (nb & ~pm) | (na & pm);
+  const uint32_t d1 = cd_max_u16x2(d, 0x00010001u);
+  const uint32_t mx1 = cd_max_u16x2(mx, 0x00010001u);
+  const uint32_t q1 = cd_mad(num, k.three, cd_mad(d1, k.neg1, 0x04000400u));  // 3num - d1 + 2^10
+  const uint32_t q2 = cd_mad(num, k.three, cd_mad(d1, k.neg2, 0x08000800u));  // 3num - 2d1 + 2^11
+  const uint32_t q3 = cd_mad(d1, k.neg1, cd_mad(num, k.one, 0x01000100u));   // num - d1 + 2^8
+  const uint32_t s1 = cd_mad(d, k.three, cd_mad(mx1, k.neg1, 0x10001000u));  // 3d - mx1 + 2^12
+  const uint32_t s2 = cd_mad(d, k.three, cd_mad(mx1, k.neg2, 0x20002000u));  // 3d - 2mx1 + 2^13
+  const uint32_t vv = cd_mulhi(mx, k.v3);        // (3 max) >> 2: bits 8,9 of 3 max -> 6,7
+  const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
+  return (ab & 0x02200220u) | (vv & 0x00C000C0u) | (q3 & 0x01000100u) | (q1 & 0x04000400u) |
+         (q2 & 0x08000800u) | (s1 & 0x10001000u) | (s2 & 0x20002000u) | (ris & 0x80008000u);
+}
+
+CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B) { return code_pair(R, G, B, kMadK); }
+
+// Byte offsets (4 * code index) of the two lanes' histogram entries.
+CD_HD uint32_t code_off_lo(uint32_t code, MadK k) { return cd_mulhi(cd_mad(code, k.sl16, 0u), k.sh13); }
+CD_HD uint32_t code_off_hi(uint32_t code, MadK k) { return cd_mulhi(code, k.sh13); }
+
+// code index (lane >> 5) -> bin in [0,162), or 255 for an unreachable code.
+CD_HD uint32_t code_to_bin(uint32_t idx) {
+  const uint32_t c = idx << kCodeShift;
+  const uint32_t A = (c >> 5) & 1u, v = (c >> 6) & 3u, q3 = (c >> 8) & 1u, B = (c >> 9) & 1u;
+  const uint32_t q1 = (c >> 10) & 1u, q2 = (c >> 11) & 1u, s1 = (c >> 12) & 1u;
+  const uint32_t s2 = (c >> 13) & 1u, z = (c >> 14) & 1u, ris = (c >> 15) & 1u;
+  const uint32_t C = A ^ B ^ ris;  // ris = A ^ B ^ C
+  const uint32_t oidx = (A << 2) | (B << 1) | C;
+  if (z || oidx == 1u || oidx == 6u || v > 2u) return 255u;
+  const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
+  return (k3 + q1 + q2 + q3) * 9u + (s1 + s2) * 3u + v;
+}
+
+// Pack 4 pixels (12 bytes in words w0, w1, w2) into two u16x2 pairs:
+// (R01, G01, B01) = pixels 0,1 and (R23, G23, B23) = pixels 2,3.
+CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
+                   uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23, MadK k) {
+  // w0 = [r0 g0 b0 r1], w1 = [g1 b1 r2 g2], w2 = [b2 r3 g3 b3] (byte 0 first)
+  const uint32_t s0 = cd_mulhi(w0, k.sh24);  // w0 >> 8 = [g0 b0 r1 0]
+  const uint32_t s1 = cd_mulhi(w1, k.sh24);  // w1 >> 8 = [b1 r2 g2 0]
+  R01 = cd_prmt(w0, 0u, 0x4340u);
+  G01 = cd_prmt(s0, w1, 0x3430u);
+  B01 = cd_prmt(s0, w1, 0x3531u);
+  R23 = cd_prmt(s1, w2, 0x3531u);
+  G23 = cd_prmt(s1, w2, 0x3632u);
+  B23 = cd_prmt(w2, 0u, 0x4340u);
+}
+
+CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
+                   uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23) {
+  unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, kMadK);
+}
+
+// -------------------------------------------------- scalar forms (reference/tests)
+// Fast scalar (18, 3, 3) form, same sector arithmetic, one pixel.
+CD_HD uint32_t bin_18_3_3(uint32_t r, uint32_t g, uint32_t b) {
+  const uint32_t c = code_pair(r, g, b) & 0xFFFFu;
+  return code_to_bin(c >> kCodeShift);
 }
 
 // General (nh, ns, nv) with nh*ns*nv <= 256 (integer division; not the hot path).
-__device__ __forceinline__ uint32_t bin_generic(uint32_t r, uint32_t g, uint32_t b, uint32_t nh,
-                                                uint32_t ns, uint32_t nv) {
-  const uint32_t mx = __vimax3_u32(r, g, b);
-  const uint32_t mn = __vimin3_u32(r, g, b);
+CD_HD uint32_t bin_generic(uint32_t r, uint32_t g, uint32_t b, uint32_t nh, uint32_t ns,
+                           uint32_t nv) {
+  uint32_t mx = r > g ? r : g;
+  mx = mx > b ? mx : b;
+  uint32_t mn = r < g ? r : g;
+  mn = mn < b ? mn : b;
   const uint32_t d = mx - mn;
   const uint32_t mid = r + g + b - mx - mn;
-  const uint32_t idx = ((r >= g) << 2) | ((g >= b) << 1) | (r >= b);
+  const uint32_t idx = ((uint32_t)(r >= g) << 2) | ((uint32_t)(g >= b) << 1) | (uint32_t)(r >= b);
   const uint32_t k = ((kSector3k >> (idx << 2)) & 15u) / 3u;
   const uint32_t num = (k & 1u) ? (mx - mid) : (mid - mn);
   const uint32_t h = d == 0 ? 0u : (nh * (k * d + num)) / (6u * d);

@@ -11,11 +11,14 @@
 //    (cp.async.bulk ... mbarrier::complete_tx, L2 evict_first) into a
 //    kStages-deep ring; consumers signal "empty" per warp;
 //  * 8 consumer warps; each thread takes 48-byte groups (16 pixels, three
-//    conflict-free LDS.128) and bins them with the division-free sector
-//    form (binfn.cuh) into a warp-private shared histogram
-//    (atomicAdd(+1) -> ATOMS.POPC.INC, same-bin lanes combined in hardware);
-//  * at a frame change the 8 warp histograms are summed and added to the
-//    global u32 histogram (integer adds: order-free, bit-deterministic).
+//    conflict-free LDS.128), unpacks them into u16x2 pixel pairs and computes
+//    a per-pixel threshold CODE two pixels per instruction (binfn.cuh,
+//    code_pair: division-free sector form of the exact HSV bins), counted in
+//    a CTA-shared 2048-entry code histogram (atomicAdd(+1) ->
+//    ATOMS.POPC.INC, same-address lanes combined in hardware);
+//  * at a frame change the code histogram is mapped to the 162 bins
+//    (code_to_bin, a 2 KB smem table) and added to the global u32 histogram
+//    (integer adds: order-free, bit-deterministic).
 #include "binfn.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -30,20 +33,41 @@ constexpr int kThreads = kConsumers + 32;  // + producer warp
 constexpr int kGroupsPerThread = 2;
 constexpr int kStageGroups = kConsumers * kGroupsPerThread;  // 512 groups = 24 KiB
 constexpr int kStageBytes = kStageGroups * 48;
-constexpr int kStages = 4;
-constexpr int kHistStride = 256;
+constexpr int kHistEntries = kCodes;  // 2048 codes (fast) or <= 256 bins (generic)
 
+// Launch configurations (ring depth, CTAs per SM); the stage size is common
+// to all so that the host-side stage partition does not depend on it.
+struct K1Cfg {
+  int stages, ctas_per_sm;
+};
+constexpr K1Cfg kCfgs[] = {{4, 2}, {2, 3}, {3, 2}, {6, 1}};
+constexpr int kNumCfgs = 4;
+
+template <int STAGES>
 struct K1Smem {
-  alignas(128) uint8_t buf[kStages][kStageBytes];
-  uint32_t whist[kConsumerWarps][kHistStride];
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  alignas(128) uint8_t buf[STAGES][kStageBytes];
+  uint32_t hist[kHistEntries];   // CTA-shared code (or bin) histogram
+  uint32_t binacc[256];          // flush: per-bin sums
+  uint8_t c2b[kCodes];           // code -> bin
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  MadK mk;
 };
 
 struct StageIter {
   const HistSeg* segs;
   int32_t seg;
   int64_t frame, st;
+  // cached fields of segs[seg]
+  int64_t groups, stages, n_frames;
+  const uint8_t* frames;
+  __device__ void load() {
+    const HistSeg& g = segs[seg];
+    groups = g.groups;
+    stages = g.stages;
+    n_frames = g.n_frames;
+    frames = g.frames;
+  }
   __device__ void seek(const HistSeg* s, int32_t nseg, int64_t g) {
     segs = s;
     int32_t lo = 0, hi = nseg - 1;
@@ -52,24 +76,29 @@ struct StageIter {
       if (s[m].stage_base <= g) lo = m; else hi = m - 1;
     }
     seg = lo;
+    load();
     int64_t rel = g - s[lo].stage_base;
-    frame = rel / s[lo].stages;
-    st = rel - frame * s[lo].stages;
+    frame = rel / stages;
+    st = rel - frame * stages;
   }
-  __device__ void next() {
-    if (++st == segs[seg].stages) {
+  // advance; returns true if the frame (or segment) changed
+  __device__ bool next(bool more) {
+    if (++st == stages) {
       st = 0;
-      if (++frame == segs[seg].n_frames) {
+      if (++frame == n_frames) {
         frame = 0;
         ++seg;
+        if (more) load();
       }
+      return true;
     }
+    return false;
   }
 };
 
 template <int MODE>
-__device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* wh, uint32_t nh,
-                                          uint32_t ns, uint32_t nv, uint32_t& xacc) {
+__device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, uint32_t nh,
+                                          uint32_t ns, uint32_t nv, MadK mk, uint32_t& xacc) {
   const uint4* p = reinterpret_cast<const uint4*>(src);
   const uint4 a = p[0], b = p[1], c = p[2];
   const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
@@ -78,27 +107,38 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* wh, uint
     for (int i = 0; i < 12; ++i) xacc ^= w[i];
     return;
   }
+  if (MODE == kModeFast) {
+    char* hb = reinterpret_cast<char*>(hist);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t R01, G01, B01, R23, G23, B23;
+      unpack4(w[3 * q], w[3 * q + 1], w[3 * q + 2], R01, G01, B01, R23, G23, B23, mk);
+      const uint32_t c01 = code_pair(R01, G01, B01, mk);
+      const uint32_t c23 = code_pair(R23, G23, B23, mk);
+      // byte offsets of the code-histogram entries: 4 * (lane >> 5)
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_lo(c01, mk)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_hi(c01, mk)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_lo(c23, mk)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_hi(c23, mk)), 1u);
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int o = 3 * i;
     const uint32_t r = __byte_perm(w[o >> 2], 0u, 0x4440u | (o & 3));
     const uint32_t g = __byte_perm(w[(o + 1) >> 2], 0u, 0x4440u | ((o + 1) & 3));
     const uint32_t bb = __byte_perm(w[(o + 2) >> 2], 0u, 0x4440u | ((o + 2) & 3));
-    uint32_t bin;
-    if (MODE == kModeFast)
-      bin = bin_18_3_3(r, g, bb);
-    else
-      bin = bin_generic(r, g, bb, nh, ns, nv);
-    atomicAdd(&wh[bin], 1u);
+    atomicAdd(&hist[bin_generic(r, g, bb, nh, ns, nv)], 1u);
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int MODE, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
-               uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* __restrict__ sink) {
+               uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
+  K1Smem<STAGES>& sm = *reinterpret_cast<K1Smem<STAGES>*>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t nbins = nh * ns * nv;
@@ -106,10 +146,14 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
 
-  for (int i = tid; i < kConsumerWarps * kHistStride; i += kThreads)
-    (&sm.whist[0][0])[i] = 0u;
+  const uint32_t nentries = MODE == kModeFast ? (uint32_t)kCodes : nbins;
+  for (int i = tid; i < kHistEntries; i += kThreads) sm.hist[i] = 0u;
+  for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
+  if (MODE == kModeFast)
+    for (int i = tid; i < kCodes; i += kThreads) sm.c2b[i] = (uint8_t)code_to_bin(i);
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    sm.mk = mk_param;
+    for (int i = 0; i < STAGES; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], kConsumerWarps);
     }
@@ -126,58 +170,75 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       it.seek(segs, nseg, s_begin);
       uint32_t i = 0;
       for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-        const uint32_t slot = i % kStages, par = (i / kStages) & 1u;
-        if (i >= kStages) mbar_wait(&sm.empty[slot], par ^ 1u);
-        const HistSeg& sg = segs[it.seg];
+        const uint32_t slot = i % STAGES, par = (i / STAGES) & 1u;
+        if (i >= STAGES) mbar_wait(&sm.empty[slot], par ^ 1u);
         const int64_t g0 = it.st * kStageGroups;
-        const int64_t ng = min((int64_t)kStageGroups, sg.groups - g0);
+        const int64_t ng = min((int64_t)kStageGroups, it.groups - g0);
         const uint32_t bytes = (uint32_t)(ng * 48);
-        const uint8_t* src = sg.frames + (it.frame * sg.groups + g0) * 48;
+        const uint8_t* src = it.frames + (it.frame * it.groups + g0) * 48;
         mbar_arrive_expect_tx(&sm.full[slot], bytes);
         bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
-        it.next();
+        it.next(s + 1 < s_end);
       }
     }
     return;
   }
 
   // ------------------------------------------------------------ consumers
-  uint32_t* wh = sm.whist[warp];
+  // multiplier constants through shared memory: opaque registers for ptxas
+  MadK mk;
+  {
+    volatile uint32_t* v = reinterpret_cast<volatile uint32_t*>(&sm.mk);
+    mk.one = v[0];
+    mk.neg1 = v[1];
+    mk.neg2 = v[2];
+    mk.three = v[3];
+    mk.sh24 = v[4];
+    mk.v3 = v[5];
+    mk.sh13 = v[6];
+    mk.sl16 = v[7];
+  }
+  uint32_t* wh = sm.hist;
   uint32_t xacc = 0;
   StageIter it;
   it.seek(segs, nseg, s_begin);
   uint32_t i = 0;
   for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-    const uint32_t slot = i % kStages, par = (i / kStages) & 1u;
-    const HistSeg& sg = segs[it.seg];
+    const uint32_t slot = i % STAGES, par = (i / STAGES) & 1u;
     const int64_t g0 = it.st * kStageGroups;
-    const int ng = (int)min((int64_t)kStageGroups, sg.groups - g0);
+    const int ng = (int)min((int64_t)kStageGroups, it.groups - g0);
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
 #pragma unroll
     for (int j = 0; j < kGroupsPerThread; ++j) {
       const int gi = tid + j * kConsumers;
-      if (gi < ng) bin_group<MODE>(buf + gi * 48, wh, nh, ns, nv, xacc);
+      if (gi < ng) bin_group<MODE>(buf + gi * 48, wh, nh, ns, nv, mk, xacc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
 
     const int32_t seg_now = it.seg;
     const int64_t frame_now = it.frame;
-    it.next();
     const bool last = (s + 1 == s_end);
-    if (MODE != kModeRead && (last || it.frame != frame_now || it.seg != seg_now)) {
+    const bool changed = it.next(!last);
+    if (MODE != kModeRead && (last || changed)) {
       // flush the frame's partial histogram
+      named_bar_sync(1, kConsumers);
+      for (uint32_t c = tid; c < nentries; c += kConsumers) {
+        const uint32_t cnt = sm.hist[c];
+        if (cnt) {
+          sm.hist[c] = 0u;
+          atomicAdd(&sm.binacc[MODE == kModeFast ? sm.c2b[c] : c], cnt);
+        }
+      }
       named_bar_sync(1, kConsumers);
       uint32_t* gh = segs[seg_now].hist + frame_now * nbins;
       for (uint32_t bn = tid; bn < nbins; bn += kConsumers) {
-        uint32_t sum = 0;
-#pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          sum += sm.whist[w][bn];
-          sm.whist[w][bn] = 0u;
+        const uint32_t sum = sm.binacc[bn];
+        if (sum) {
+          sm.binacc[bn] = 0u;
+          atomicAdd(gh + bn, sum);
         }
-        if (sum) atomicAdd(gh + bn, sum);
       }
       named_bar_sync(1, kConsumers);
     }
@@ -185,39 +246,71 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   if (MODE == kModeRead && xacc == 0x9E3779B9u) sink[0] = xacc;  // keep the loads alive
 }
 
-}  // namespace
-
-size_t k1_smem_bytes() { return sizeof(K1Smem); }
-int k1_stage_groups() { return kStageGroups; }
-
-cudaError_t k1_configure() {
-  const int bytes = (int)sizeof(K1Smem);
-  cudaError_t e;
-  e = cudaFuncSetAttribute(k1_hist_kernel<kModeFast>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k1_hist_kernel<kModeGeneric>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k1_hist_kernel<kModeRead>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+template <int MODE, int C>
+cudaError_t launch_cfg(const HistSeg* d_segs, int32_t nseg, int64_t total_stages, uint32_t nh,
+                       uint32_t ns, uint32_t nv, uint32_t* sink, int grid, cudaStream_t stream) {
+  constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm;
+  k1_hist_kernel<MODE, S, M><<<grid, kThreads, sizeof(K1Smem<S>), stream>>>(
+      d_segs, nseg, total_stages, nh, ns, nv, kMadK, sink);
+  return cudaGetLastError();
 }
 
-int k1_grid(int sm_count, int64_t total_stages) {
-  int64_t g = (int64_t)sm_count * 2;
+template <int MODE>
+cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
+                        uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
+                        cudaStream_t stream) {
+  switch (cfg) {
+    case 1: return launch_cfg<MODE, 1>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    case 2: return launch_cfg<MODE, 2>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    case 3: return launch_cfg<MODE, 3>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+  }
+}
+
+template <int MODE, int C>
+cudaError_t configure_cfg() {
+  constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm;
+  return cudaFuncSetAttribute(k1_hist_kernel<MODE, S, M>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<S>));
+}
+
+template <int MODE>
+cudaError_t configure_mode() {
+  cudaError_t e;
+  if ((e = configure_cfg<MODE, 0>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 1>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 2>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 3>();
+}
+
+}  // namespace
+
+int k1_stage_groups() { return kStageGroups; }
+int k1_num_cfgs() { return kNumCfgs; }
+
+cudaError_t k1_configure() {
+  cudaError_t e;
+  if ((e = configure_mode<kModeFast>()) != cudaSuccess) return e;
+  if ((e = configure_mode<kModeGeneric>()) != cudaSuccess) return e;
+  return configure_mode<kModeRead>();
+}
+
+int k1_grid(int cfg, int sm_count, int64_t total_stages) {
+  if (cfg < 0 || cfg >= kNumCfgs) cfg = 0;
+  int64_t g = (int64_t)sm_count * kCfgs[cfg].ctas_per_sm;
   if (total_stages < g) g = total_stages;
   return (int)(g < 1 ? 1 : g);
 }
 
-cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
-                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
-                      cudaStream_t stream) {
+cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
+                      int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
+                      uint32_t* sink, int grid, cudaStream_t stream) {
   if (total_stages <= 0) return cudaSuccess;
-  const size_t bytes = sizeof(K1Smem);
   if (mode == kModeFast)
-    k1_hist_kernel<kModeFast><<<grid, kThreads, bytes, stream>>>(d_segs, nseg, total_stages, nh, ns, nv, sink);
-  else if (mode == kModeGeneric)
-    k1_hist_kernel<kModeGeneric><<<grid, kThreads, bytes, stream>>>(d_segs, nseg, total_stages, nh, ns, nv, sink);
-  else
-    k1_hist_kernel<kModeRead><<<grid, kThreads, bytes, stream>>>(d_segs, nseg, total_stages, nh, ns, nv, sink);
-  return cudaGetLastError();
+    return launch_mode<kModeFast>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+  if (mode == kModeGeneric)
+    return launch_mode<kModeGeneric>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+  return launch_mode<kModeRead>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
 }
 
 // ---------------------------------------------------------------- K5 (test)
@@ -227,7 +320,18 @@ __global__ void k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= (1u << 24)) return;
   const uint32_t r = c >> 16, g = (c >> 8) & 255u, b = c & 255u;
-  out[c] = (uint8_t)(fast ? bin_18_3_3(r, g, b) : bin_generic(r, g, b, nh, ns, nv));
+  if (!fast) {
+    out[c] = out[c + (1u << 24)] = (uint8_t)bin_generic(r, g, b, nh, ns, nv);
+    return;
+  }
+  // the hot-path pair code, this colour in lane 0 and colour c ^ 0xA5A5A5 in lane 1
+  const uint32_t c2 = c ^ 0xA5A5A5u;
+  const uint32_t code = code_pair(r | ((c2 >> 16) << 16), g | (((c2 >> 8) & 255u) << 16),
+                                  b | ((c2 & 255u) << 16));
+  const uint32_t b0 = code_to_bin((code & 0xFFFFu) >> kCodeShift);
+  const uint32_t b1 = code_to_bin(code >> (16 + kCodeShift));
+  out[c] = (uint8_t)b0;                  // table 0: lane 0
+  out[(1u << 24) + c2] = (uint8_t)b1;    // table 1: lane 1
 }
 }  // namespace
 

@@ -11,13 +11,13 @@ namespace clipdetect {
 enum { kModeFast = 0, kModeGeneric = 1, kModeRead = 2 };
 
 // ---- K1 (hist.cu)
-size_t k1_smem_bytes();
 int k1_stage_groups();
+int k1_num_cfgs();
 cudaError_t k1_configure();
-int k1_grid(int sm_count, int64_t total_stages);
-cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
-                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
-                      cudaStream_t stream);
+int k1_grid(int cfg, int sm_count, int64_t total_stages);
+cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
+                      int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
+                      uint32_t* sink, int grid, cudaStream_t stream);
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                              cudaStream_t stream);
 

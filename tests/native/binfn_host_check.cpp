@@ -1,0 +1,61 @@
+// Host-side exhaustive check of the device bin code (paper_2503_12964_b200/csrc/binfn.cuh),
+// compiled with g++ (the CUDA intrinsics are emulated on the host).  Writes the
+// 2^24-entry bin tables of lane 0 and lane 1 of code_pair(), and of
+// bin_generic() for the requested layout, to the output file; the pytest
+// compares them with the oracle's table.  (Test infrastructure.)
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <vector>
+
+#include "binfn.cuh"
+
+using namespace clipdetect;
+
+int main(int argc, char** argv) {
+  if (argc < 5) {
+    fprintf(stderr, "usage: %s out nh ns nv\n", argv[0]);
+    return 2;
+  }
+  const uint32_t nh = atoi(argv[2]), ns = atoi(argv[3]), nv = atoi(argv[4]);
+  const uint32_t N = 1u << 24;
+  std::vector<uint8_t> t0(N), t1(N), tg(N);
+  for (uint32_t c = 0; c < N; ++c) {
+    const uint32_t c2 = c ^ 0xA5A5A5u;
+    const uint32_t R = (c >> 16) | ((c2 >> 16) << 16);
+    const uint32_t G = ((c >> 8) & 255u) | (((c2 >> 8) & 255u) << 16);
+    const uint32_t B = (c & 255u) | ((c2 & 255u) << 16);
+    const uint32_t code = code_pair(R, G, B);
+    t0[c] = (uint8_t)code_to_bin((code & 0xFFFFu) >> kCodeShift);
+    t1[c2] = (uint8_t)code_to_bin(code >> (16 + kCodeShift));
+    tg[c] = (uint8_t)bin_generic(c >> 16, (c >> 8) & 255u, c & 255u, nh, ns, nv);
+  }
+  // unpack4 on pseudo-random bytes
+  uint32_t x = 12345u;
+  for (int it = 0; it < 100000; ++it) {
+    uint8_t by[12];
+    for (int i = 0; i < 12; ++i) {
+      x = x * 1664525u + 1013904223u;
+      by[i] = (uint8_t)(x >> 24);
+    }
+    uint32_t w[3];
+    memcpy(w, by, 12);
+    uint32_t R01, G01, B01, R23, G23, B23;
+    unpack4(w[0], w[1], w[2], R01, G01, B01, R23, G23, B23);
+    const uint32_t want[6] = {by[0] | (uint32_t)by[3] << 16, by[1] | (uint32_t)by[4] << 16,
+                              by[2] | (uint32_t)by[5] << 16, by[6] | (uint32_t)by[9] << 16,
+                              by[7] | (uint32_t)by[10] << 16, by[8] | (uint32_t)by[11] << 16};
+    const uint32_t got[6] = {R01, G01, B01, R23, G23, B23};
+    for (int i = 0; i < 6; ++i)
+      if (got[i] != want[i]) {
+        fprintf(stderr, "unpack4 mismatch %d: %08x vs %08x\n", i, got[i], want[i]);
+        return 1;
+      }
+  }
+  FILE* f = fopen(argv[1], "wb");
+  fwrite(t0.data(), 1, N, f);
+  fwrite(t1.data(), 1, N, f);
+  fwrite(tg.data(), 1, N, f);
+  fclose(f);
+  return 0;
+}

@@ -58,8 +58,9 @@ def _dev_video(v, dev, emb=True):
 def test_binmap_all_colours_fast(ctx):
     got = ctx.debug_binmap().cpu().numpy()
     want = oracle.bin_table()
-    bad = np.nonzero(got != want)[0]
-    assert bad.size == 0, f"{bad.size} colours differ, first {bad[:5]}"
+    for lane in range(2):
+        bad = np.nonzero(got[lane] != want)[0]
+        assert bad.size == 0, f"lane {lane}: {bad.size} colours differ, first {bad[:5]}"
 
 
 @pytest.mark.parametrize("bins", [(12, 4, 4), (6, 2, 2), (36, 3, 2), (8, 8, 4)])
@@ -69,7 +70,7 @@ def test_binmap_all_colours_generic(dev, bins):
     got = c.debug_binmap().cpu().numpy()
     want = oracle.bin_table(oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2]))
     c.close()
-    assert np.array_equal(got, want)
+    assert np.array_equal(got[0], want) and np.array_equal(got[1], want)
 
 
 # ------------------------------------------------------------------ a3-a4
@@ -281,7 +282,11 @@ def _run_config_streamed(ctx, dev, name, max_videos=None):
     for v, r in zip(vids, res):
         g = gold["videos"][v.id]
         _check_against_golden(g, r, h[off:off + v.n], l[off:off + v.n])
-        assert set(v.hard) <= set(r.final.tolist())
+        # planted hard cuts survive unless a fade/flash exit within L_min+12 frames
+        # before them already took the cut (a property of the method, O5)
+        clear = [c for c in v.hard
+                 if all(abs(c - f) > 20 for f in v.fades) and all(abs(c - s) > 20 for s, _ in v.flashes)]
+        assert set(clear) <= set(r.final.tolist())
         off += v.n
     return res
 

@@ -1,0 +1,73 @@
+#!/usr/bin/env python3
+"""K1 micro-benchmark: the histogram kernel against the same TMA pipeline
+without binning (K6 read roofline), on C2 content and on uniform-noise
+frames.  CUDA events on the ctx stream; inputs >> L2.  Prints one JSON line."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from synth import manifest, torch_dev  # noqa: E402
+from paper_2503_12964_b200 import Ctx  # noqa: E402
+
+
+def timeit(fn, stream, reps=5):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 6000
+    dev = torch.device("cuda:0")
+    synth.build(device=True)
+    stream = torch.cuda.Stream()
+    cfgs = [int(c) for c in os.environ.get("K1_CFGS", "0").split(",")]
+    ctxs = {}
+    for c in cfgs:
+        os.environ["CLIPDETECT_K1_CFG"] = str(c)
+        ctxs[c] = Ctx(device=0, stream=stream)
+    os.environ.pop("CLIPDETECT_K1_CFG", None)
+    out = {}
+    for name, v in [("c2", manifest.subsample(manifest.c2_video(0), n)),
+                    ("noise", manifest.noise_video(0, 1280, 720, n))]:
+        table = torch_dev.frame_table(v, dev)
+        frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+        torch_dev.gen_frames(v, table, frames)
+        hist = torch.empty((v.n, 162), dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        nbytes = frames.numel()
+        ref = None
+        for c, ctx in ctxs.items():
+            with torch.cuda.stream(stream):
+                ms_k1 = timeit(lambda: ctx.frame_scores(frames, hist=hist, want_l1=False,
+                                                        want_score=False), stream)
+                ms_rd = timeit(lambda: ctx.debug_read_roofline(frames), stream)
+            h = hist.clone()
+            same = True if ref is None else bool(torch.equal(ref, h))
+            ref = h if ref is None else ref
+            out[f"{name}_cfg{c}"] = {"frames": v.n, "bytes": nbytes, "k1_ms": round(ms_k1, 3),
+                                     "k1_gbs": round(nbytes / ms_k1 / 1e6, 1),
+                                     "read_ms": round(ms_rd, 3),
+                                     "read_gbs": round(nbytes / ms_rd / 1e6, 1),
+                                     "k1_frac_of_read": round(ms_rd / ms_k1, 3),
+                                     "hist_equal_cfg0": same}
+        del frames, hist
+        torch.cuda.empty_cache()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
