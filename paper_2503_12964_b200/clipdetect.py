@@ -79,12 +79,13 @@ def load(build_if_missing: bool = False):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("CLIPDETECT_LIB", LIB_PATH)  # experiment builds (tools/) only
+    if not os.path.exists(path):
         if build_if_missing:
             _build.build()
         else:
-            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(path)
     vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.clip_params_default.argtypes = [ctypes.POINTER(ClipParams)]
     L.clip_params_default.restype = None

@@ -108,13 +108,15 @@ constexpr int kCodes = 1 << (16 - kCodeShift);  // 2048
 // the FMA pipe and leaves the ALU pipe (LOP3/PRMT/VIMNMX/SHF, the binding
 // pipe on sm_100) to the bit work.
 struct MadK {
-  uint32_t one, neg1, neg2, three;
+  uint32_t one, neg1, neg2, three, four;
+  uint32_t sl8;    // 2^8
+  uint32_t sl24;   // 2^24
   uint32_t sh24;   // 2^24: mulhi(x, sh24) = x >> 8
   uint32_t v3;     // 3 * 2^30: mulhi(x, v3) = (3x) >> 2
   uint32_t sh13;   // 2^13: mulhi(x, sh13) = x >> 19
   uint32_t sl16;   // 2^16: x * sl16 = x << 16
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 4u, 1u << 8, 1u << 24, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -183,6 +185,64 @@ CD_HD uint32_t code_to_bin(uint32_t idx) {
   if (z || oidx == 1u || oidx == 6u || v > 2u) return 255u;
   const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
   return (k3 + q1 + q2 + q3) * 9u + (s1 + s2) * 3u + v;
+}
+
+// ------------------------------------------------------------ LUT variant
+// The in-sector hue offsets come from a 64 KiB shared-memory table instead of
+// three threshold tests and a select:
+//   lut[d*256 + (na ^ (4d & 0xFC))] = qr | qf << 2,
+//   qr = floor(3 na / d) (rising sectors), qf = floor(3 (d - na) / d) (falling),
+// na = mid - min, d = max - min (0 for grey).  The XOR swizzle spreads equal-na
+// lanes over the 32 banks.  Lane code layout:
+//   bit 5 A, bits 6-7 v, bits 8-9 qr, bits 10-11 qf, bit 12 s1, bit 13 s2,
+//   bit 14 B, bit 15 ris.
+CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
+  if (d == 0) return 0u;
+  const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
+  return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
+}
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d) { return d * 256u + (na ^ ((4u * d) & 0xFCu)); }
+
+// Part 1 (before the table lookups): returns the partial code and the two
+// lanes' table indices.
+CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
+                                 uint32_t& i1) {
+  constexpr uint32_t kB15 = 0x80008000u;
+  const uint32_t mx = cd_max3_u16x2(R, G, B);
+  const uint32_t mn = cd_min3_u16x2(R, G, B);
+  const uint32_t d = cd_mad(mn, k.neg1, mx);
+  const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, R + G + B));  // mid - min
+  const uint32_t nas = na ^ (cd_mad(d, k.four, 0u) & 0x00FC00FCu);         // swizzle
+  i0 = cd_prmt(nas, d, 0x1140u);  // lane 0: nas | d << 8
+  i1 = cd_prmt(nas, d, 0x3362u);  // lane 1
+  const uint32_t R15 = cd_mad(R, k.one, kB15);
+  const uint32_t tA = cd_mad(G, k.neg1, R15);                     // bit 15: r >= g
+  const uint32_t tB = cd_mad(B, k.neg1, cd_mad(G, k.one, kB15));  // bit 15: g >= b
+  const uint32_t tC = cd_mad(B, k.neg1, R15);                     // bit 15: r >= b
+  const uint32_t ris = tA ^ tB ^ tC;                              // bit 15: rising sector
+  const uint32_t mx1 = cd_max_u16x2(mx, 0x00010001u);
+  const uint32_t z1 = cd_mad(mx1, k.neg1, 0x10001000u);
+  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx1 + 2^12
+  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx1 + 2^13
+  const uint32_t vv = cd_mulhi(mx, k.v3);      // bits 8,9 of 3 max -> 6,7
+  const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
+  return (ab & 0x40204020u) | (vv & 0x00C000C0u) | (s1 & 0x10001000u) | (s2 & 0x20002000u) |
+         (ris & 0x80008000u);
+}
+// Part 2: add the two looked-up entries (q0 for lane 0, q1 for lane 1).
+CD_HD uint32_t code_pair_lut_post(uint32_t pre, uint32_t q0, uint32_t q1, MadK k) {
+  return cd_mad(q1, k.sl24, cd_mad(q0, k.sl8, pre));
+}
+
+CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
+  const uint32_t c = idx << kCodeShift;
+  const uint32_t A = (c >> 5) & 1u, v = (c >> 6) & 3u, qr = (c >> 8) & 3u, qf = (c >> 10) & 3u;
+  const uint32_t s1 = (c >> 12) & 1u, s2 = (c >> 13) & 1u, B = (c >> 14) & 1u, ris = (c >> 15) & 1u;
+  const uint32_t C = A ^ B ^ ris;
+  const uint32_t oidx = (A << 2) | (B << 1) | C;
+  if (oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
+  const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
+  return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
 }
 
 // Pack 4 pixels (12 bytes in words w0, w1, w2) into two u16x2 pairs:

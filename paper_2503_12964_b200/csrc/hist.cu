@@ -27,28 +27,26 @@ namespace clipdetect {
 
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;  // + producer warp
-constexpr int kGroupsPerThread = 2;
-constexpr int kStageGroups = kConsumers * kGroupsPerThread;  // 512 groups = 24 KiB
+constexpr int kStageGroups = 512;  // 48-byte groups per stage (24 KiB), common to all configs
 constexpr int kStageBytes = kStageGroups * 48;
 constexpr int kHistEntries = kCodes;  // 2048 codes (fast) or <= 256 bins (generic)
+constexpr int kLutBytes = 65536;
 
-// Launch configurations (ring depth, CTAs per SM); the stage size is common
-// to all so that the host-side stage partition does not depend on it.
+// Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
 struct K1Cfg {
-  int stages, ctas_per_sm;
+  int stages, ctas_per_sm, warps, lut;
 };
-constexpr K1Cfg kCfgs[] = {{4, 2}, {2, 3}, {3, 2}, {6, 1}};
-constexpr int kNumCfgs = 4;
+constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0}, {2, 3, 8, 0}, {3, 2, 8, 0}, {6, 1, 8, 0},
+                           {4, 1, 16, 1}, {2, 1, 16, 1}, {4, 1, 16, 0}};
+constexpr int kNumCfgs = 7;
 
-template <int STAGES>
+template <int STAGES, int LUT>
 struct K1Smem {
   alignas(128) uint8_t buf[STAGES][kStageBytes];
-  uint32_t hist[kHistEntries];   // CTA-shared code (or bin) histogram
-  uint32_t binacc[256];          // flush: per-bin sums
-  uint8_t c2b[kCodes];           // code -> bin
+  uint8_t lut[LUT ? kLutBytes : 16];
+  uint32_t hist[kHistEntries];  // CTA-shared code (or bin) histogram
+  uint32_t binacc[256];         // flush: per-bin sums
+  uint8_t c2b[kCodes];          // code -> bin
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   MadK mk;
@@ -96,9 +94,22 @@ struct StageIter {
   }
 };
 
-template <int MODE>
-__device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, uint32_t nh,
-                                          uint32_t ns, uint32_t nv, MadK mk, uint32_t& xacc) {
+#ifdef CLIPDETECT_EXP_NO_ATOMS
+// experiment build only (tools/): keep the codes alive without the histogram atomics
+__device__ uint32_t g_exp_sink;
+__device__ __forceinline__ void hist_inc(char* hb, uint32_t off) {
+  if (off == 0xFFFFFFFFu) g_exp_sink = off;
+}
+#else
+__device__ __forceinline__ void hist_inc(char* hb, uint32_t off) {
+  atomicAdd(reinterpret_cast<uint32_t*>(hb + off), 1u);
+}
+#endif
+
+template <int MODE, int LUT>
+__device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, const uint8_t* lut,
+                                          uint32_t nh, uint32_t ns, uint32_t nv, MadK mk,
+                                          uint32_t& xacc) {
   const uint4* p = reinterpret_cast<const uint4*>(src);
   const uint4 a = p[0], b = p[1], c = p[2];
   const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
@@ -113,13 +124,22 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, ui
     for (int q = 0; q < 4; ++q) {
       uint32_t R01, G01, B01, R23, G23, B23;
       unpack4(w[3 * q], w[3 * q + 1], w[3 * q + 2], R01, G01, B01, R23, G23, B23, mk);
-      const uint32_t c01 = code_pair(R01, G01, B01, mk);
-      const uint32_t c23 = code_pair(R23, G23, B23, mk);
+      uint32_t c01, c23;
+      if (LUT) {
+        uint32_t a0, a1, b0, b1;
+        const uint32_t p01 = code_pair_lut_pre(R01, G01, B01, mk, a0, a1);
+        const uint32_t p23 = code_pair_lut_pre(R23, G23, B23, mk, b0, b1);
+        c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
+        c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
+      } else {
+        c01 = code_pair(R01, G01, B01, mk);
+        c23 = code_pair(R23, G23, B23, mk);
+      }
       // byte offsets of the code-histogram entries: 4 * (lane >> 5)
-      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_lo(c01, mk)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_hi(c01, mk)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_lo(c23, mk)), 1u);
-      atomicAdd(reinterpret_cast<uint32_t*>(hb + code_off_hi(c23, mk)), 1u);
+      hist_inc(hb, code_off_lo(c01, mk));
+      hist_inc(hb, code_off_hi(c01, mk));
+      hist_inc(hb, code_off_lo(c23, mk));
+      hist_inc(hb, code_off_hi(c23, mk));
     }
     return;
   }
@@ -133,12 +153,17 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, ui
   }
 }
 
-template <int MODE, int STAGES, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <int MODE, int STAGES, int MINB, int CW, int LUT>
+__global__ void __launch_bounds__(CW * 32 + 32, MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
+  constexpr int kConsumers = CW * 32;
+  constexpr int kThreads = kConsumers + 32;
+  constexpr int kGPT = kStageGroups / kConsumers;
+  static_assert(kGPT * kConsumers == kStageGroups, "stage must split evenly");
+  constexpr bool kUseLut = (MODE == kModeFast) && LUT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  K1Smem<STAGES>& sm = *reinterpret_cast<K1Smem<STAGES>*>(smem_raw);
+  K1Smem<STAGES, LUT>& sm = *reinterpret_cast<K1Smem<STAGES, LUT>*>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t nbins = nh * ns * nv;
@@ -150,19 +175,26 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   for (int i = tid; i < kHistEntries; i += kThreads) sm.hist[i] = 0u;
   for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
   if (MODE == kModeFast)
-    for (int i = tid; i < kCodes; i += kThreads) sm.c2b[i] = (uint8_t)code_to_bin(i);
+    for (int i = tid; i < kCodes; i += kThreads)
+      sm.c2b[i] = (uint8_t)(kUseLut ? code_to_bin_lut(i) : code_to_bin(i));
+  if (kUseLut)
+    for (int i = tid; i < kLutBytes; i += kThreads) {
+      const uint32_t d = (uint32_t)i >> 8, nas = (uint32_t)i & 255u;
+      const uint32_t na = nas ^ ((4u * d) & 0xFCu);
+      sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+    }
   if (tid == 0) {
     sm.mk = mk_param;
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kConsumerWarps);
+      mbar_init(&sm.empty[i], CW);
     }
     fence_mbar_init();
   }
   __syncthreads();
   if (s_begin >= s_end) return;
 
-  if (warp == kConsumerWarps) {
+  if (warp == CW) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -188,15 +220,10 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   // multiplier constants through shared memory: opaque registers for ptxas
   MadK mk;
   {
-    volatile uint32_t* v = reinterpret_cast<volatile uint32_t*>(&sm.mk);
-    mk.one = v[0];
-    mk.neg1 = v[1];
-    mk.neg2 = v[2];
-    mk.three = v[3];
-    mk.sh24 = v[4];
-    mk.v3 = v[5];
-    mk.sh13 = v[6];
-    mk.sl16 = v[7];
+    const volatile uint32_t* v = reinterpret_cast<const volatile uint32_t*>(&sm.mk);
+    uint32_t* m = reinterpret_cast<uint32_t*>(&mk);
+#pragma unroll
+    for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t* wh = sm.hist;
   uint32_t xacc = 0;
@@ -210,9 +237,9 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
 #pragma unroll
-    for (int j = 0; j < kGroupsPerThread; ++j) {
+    for (int j = 0; j < kGPT; ++j) {
       const int gi = tid + j * kConsumers;
-      if (gi < ng) bin_group<MODE>(buf + gi * 48, wh, nh, ns, nv, mk, xacc);
+      if (gi < ng) bin_group<MODE, LUT>(buf + gi * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -247,11 +274,19 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 }
 
 template <int MODE, int C>
+struct Cfg {
+  static constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm, W = kCfgs[C].warps,
+                       L = kCfgs[C].lut;
+  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L>; }
+  static constexpr size_t smem() { return sizeof(K1Smem<S, L>); }
+};
+
+template <int MODE, int C>
 cudaError_t launch_cfg(const HistSeg* d_segs, int32_t nseg, int64_t total_stages, uint32_t nh,
                        uint32_t ns, uint32_t nv, uint32_t* sink, int grid, cudaStream_t stream) {
-  constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm;
-  k1_hist_kernel<MODE, S, M><<<grid, kThreads, sizeof(K1Smem<S>), stream>>>(
-      d_segs, nseg, total_stages, nh, ns, nv, kMadK, sink);
+  using K = Cfg<MODE, C>;
+  K::kernel()<<<grid, K::W * 32 + 32, K::smem(), stream>>>(d_segs, nseg, total_stages, nh, ns,
+                                                             nv, kMadK, sink);
   return cudaGetLastError();
 }
 
@@ -259,19 +294,20 @@ template <int MODE>
 cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
                         uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
                         cudaStream_t stream) {
+#define K1_CASE(c) \
+  case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   switch (cfg) {
-    case 1: return launch_cfg<MODE, 1>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-    case 2: return launch_cfg<MODE, 2>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-    case 3: return launch_cfg<MODE, 3>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
+#undef K1_CASE
 }
 
 template <int MODE, int C>
 cudaError_t configure_cfg() {
-  constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm;
-  return cudaFuncSetAttribute(k1_hist_kernel<MODE, S, M>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem<S>));
+  using K = Cfg<MODE, C>;
+  return cudaFuncSetAttribute(K::kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)K::smem());
 }
 
 template <int MODE>
@@ -280,7 +316,10 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 0>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 1>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 2>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 3>();
+  if ((e = configure_cfg<MODE, 3>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 4>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 5>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 6>();
 }
 
 }  // namespace

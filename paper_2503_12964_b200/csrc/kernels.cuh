@@ -53,7 +53,7 @@ struct MergeVideo {
   int32_t clip_base;   // first global clip index
   int32_t n_clips;     // n_cuts + 1
 };
-constexpr int kPieceFrames = 256;
+constexpr int kPieceFrames = 16;  // frames per piece-sum CTA (parallelism over the frame axis)
 
 struct MergeScratch {
   int32_t* clip_video;  // [K]

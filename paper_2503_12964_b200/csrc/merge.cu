@@ -10,7 +10,7 @@
 //  together".)
 //
 // Determinism: every sum runs in a fixed order (frames ascending inside a
-// <=256-frame piece, pieces ascending inside a clip, clips ascending inside a
+// <=16-frame piece, pieces ascending inside a clip, clips ascending inside a
 // merged range, fixed shuffle trees for the dot products); no float atomics.
 // The oracle sums a merged clip frame by frame, the device piece by piece:
 // same terms, different association (~1e-16 relative).
@@ -124,7 +124,8 @@ __device__ __forceinline__ int32_t find_piece_clip(const int32_t* __restrict__ p
   return lo;
 }
 
-// P[p][d] = sum of frames of piece p (f64, ascending frames)
+// P[p][d] = sum of frames of piece p (f64, ascending frames); float4 loads
+// when the rows allow it (D = 768: 192 threads x 4 dims)
 __global__ void __launch_bounds__(kT)
 k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, MergeScratch s) {
   const int64_t p = blockIdx.x;
@@ -134,21 +135,31 @@ k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, M
   const int32_t f0 = s.clip_f0[k] + i * kPieceFrames;
   const int32_t f1 = min(s.clip_f1[k], f0 + kPieceFrames);
   const float* __restrict__ e = mv[s.clip_video[k]].emb;
+  double* __restrict__ out = s.P + p * dim;
+  if ((dim & 3) == 0 && (reinterpret_cast<uintptr_t>(e) & 15) == 0) {
+    const int32_t d4n = dim >> 2;
+    for (int32_t d4 = threadIdx.x; d4 < d4n; d4 += kT) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const float4* src = reinterpret_cast<const float4*>(e + (int64_t)f0 * dim) + d4;
+#pragma unroll 4
+      for (int32_t f = f0; f < f1; ++f) {
+        const float4 x = __ldg(src);
+        src += d4n;
+        a0 += (double)x.x;
+        a1 += (double)x.y;
+        a2 += (double)x.z;
+        a3 += (double)x.w;
+      }
+      double2* o = reinterpret_cast<double2*>(out + 4 * d4);
+      o[0] = make_double2(a0, a1);
+      o[1] = make_double2(a2, a3);
+    }
+    return;
+  }
   for (int32_t d = threadIdx.x; d < dim; d += kT) {
     double acc = 0.0;
-    int32_t f = f0;
-    for (; f + 4 <= f1; f += 4) {
-      const float a0 = __ldg(e + (int64_t)f * dim + d);
-      const float a1 = __ldg(e + (int64_t)(f + 1) * dim + d);
-      const float a2 = __ldg(e + (int64_t)(f + 2) * dim + d);
-      const float a3 = __ldg(e + (int64_t)(f + 3) * dim + d);
-      acc += (double)a0;
-      acc += (double)a1;
-      acc += (double)a2;
-      acc += (double)a3;
-    }
-    for (; f < f1; ++f) acc += (double)__ldg(e + (int64_t)f * dim + d);
-    s.P[p * dim + d] = acc;
+    for (int32_t f = f0; f < f1; ++f) acc += (double)__ldg(e + (int64_t)f * dim + d);
+    out[d] = acc;
   }
 }
 

@@ -19,7 +19,10 @@ int main(int argc, char** argv) {
   }
   const uint32_t nh = atoi(argv[2]), ns = atoi(argv[3]), nv = atoi(argv[4]);
   const uint32_t N = 1u << 24;
-  std::vector<uint8_t> t0(N), t1(N), tg(N);
+  std::vector<uint8_t> t0(N), t1(N), tg(N), l0(N), l1(N);
+  std::vector<uint8_t> lut(65536, 0);
+  for (uint32_t d = 0; d < 256; ++d)
+    for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d)] = (uint8_t)lut_entry(na, d);
   for (uint32_t c = 0; c < N; ++c) {
     const uint32_t c2 = c ^ 0xA5A5A5u;
     const uint32_t R = (c >> 16) | ((c2 >> 16) << 16);
@@ -29,6 +32,11 @@ int main(int argc, char** argv) {
     t0[c] = (uint8_t)code_to_bin((code & 0xFFFFu) >> kCodeShift);
     t1[c2] = (uint8_t)code_to_bin(code >> (16 + kCodeShift));
     tg[c] = (uint8_t)bin_generic(c >> 16, (c >> 8) & 255u, c & 255u, nh, ns, nv);
+    uint32_t i0, i1;
+    const uint32_t pre = code_pair_lut_pre(R, G, B, kMadK, i0, i1);
+    const uint32_t lc = code_pair_lut_post(pre, lut[i0], lut[i1], kMadK);
+    l0[c] = (uint8_t)code_to_bin_lut((lc & 0xFFFFu) >> kCodeShift);
+    l1[c2] = (uint8_t)code_to_bin_lut(lc >> (16 + kCodeShift));
   }
   // unpack4 on pseudo-random bytes
   uint32_t x = 12345u;
@@ -56,6 +64,8 @@ int main(int argc, char** argv) {
   fwrite(t0.data(), 1, N, f);
   fwrite(t1.data(), 1, N, f);
   fwrite(tg.data(), 1, N, f);
+  fwrite(l0.data(), 1, N, f);
+  fwrite(l1.data(), 1, N, f);
   fclose(f);
   return 0;
 }

@@ -28,10 +28,12 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
     subprocess.check_call([exe, path, *map(str, bins)])
     raw = np.fromfile(path, dtype=np.uint8)
     n = 1 << 24
-    t0, t1, tg = raw[:n], raw[n:2 * n], raw[2 * n:]
+    t0, t1, tg, l0, l1 = (raw[i * n:(i + 1) * n] for i in range(5))
     p = oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2])
     want = oracle.bin_table(p)
     assert np.array_equal(tg, want)
     if bins == (18, 3, 3):
         assert np.array_equal(t0, want), np.nonzero(t0 != want)[0][:10]
         assert np.array_equal(t1, want), np.nonzero(t1 != want)[0][:10]
+        assert np.array_equal(l0, want), np.nonzero(l0 != want)[0][:10]
+        assert np.array_equal(l1, want), np.nonzero(l1 != want)[0][:10]

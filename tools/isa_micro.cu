@@ -1,0 +1,132 @@
+// isa_micro.cu — sm_100a instruction-throughput micro-benchmark (tools only).
+// For each op: 8 independent chains per thread, N iterations, grid = 148*k CTAs
+// of 256 threads; reports warp-instructions per clock per SM (clock from
+// clock64 deltas of CTA 0).  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o isa_micro isa_micro.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t r;
+  asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t mad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t add3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) {
+  return __vimax3_u16x2(a, b, c);
+}
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+__device__ __forceinline__ uint32_t shf(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ float ffma(float a, float b, float c) {
+  float r;
+  asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+template <int OP>
+__global__ void bench(uint32_t* out, int iters, uint32_t k1, uint32_t k2, long long* clk) {
+  uint32_t x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 7 + i * 13 + blockIdx.x;
+  float f[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = (float)x[i];
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (OP == 0) x[i] = prmt(x[i], k1, 0x3210 ^ k2);
+      if (OP == 1) x[i] = lop3(x[i], k1, k2);
+      if (OP == 2) x[i] = mad(x[i], k1, k2);
+      if (OP == 3) x[i] = mulhi(x[i], k1) ^ k2;
+      if (OP == 4) x[i] = add3(x[i], k1, k2);
+      if (OP == 5) x[i] = vmax3(x[i], k1, k2);
+      if (OP == 6) x[i] = vmax2(x[i], k1);
+      if (OP == 7) x[i] = shf(x[i], k1, k2);
+      if (OP == 8) f[i] = ffma(f[i], 1.0001f, 0.5f);
+      if (OP == 9) {  // mixed: half ALU (lop3), half FMA (mad)
+        if (i & 1) x[i] = lop3(x[i], k1, k2); else x[i] = mad(x[i], k1, k2);
+      }
+      if (OP == 10) {  // mixed: 1/3 lop3, 1/3 mad, 1/3 prmt
+        if (i % 3 == 0) x[i] = lop3(x[i], k1, k2);
+        else if (i % 3 == 1) x[i] = mad(x[i], k1, k2);
+        else x[i] = prmt(x[i], k1, 0x3210 ^ k2);
+      }
+    }
+  }
+  long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= x[i] ^ __float_as_uint(f[i]);
+  if (acc == 0x12345678u) out[0] = acc;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *clk = t1 - t0;
+}
+
+template <int OP>
+void run(const char* name, int blocks_per_sm, int threads) {
+  uint32_t* out;
+  long long* clk;
+  cudaMalloc(&out, 4);
+  cudaMalloc(&clk, 8);
+  const int iters = 4096;
+  int sms = 148;
+  bench<OP><<<sms * blocks_per_sm, threads>>>(out, iters, 3u, 0u, clk);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  bench<OP><<<sms * blocks_per_sm, threads>>>(out, iters, 3u, 0u, clk);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  long long c;
+  cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
+  const double warp_instr = (double)sms * blocks_per_sm * (threads / 32) * iters * 8.0;
+  const double per_sm_per_clk = warp_instr / sms / (double)c;
+  printf("{\"op\": \"%s\", \"warps_per_sm\": %d, \"cycles\": %lld, \"ms\": %.3f, \"warp_instr_per_clk_per_sm\": %.3f}\n",
+         name, blocks_per_sm * threads / 32, c, ms, per_sm_per_clk);
+  cudaFree(out);
+  cudaFree(clk);
+}
+
+int main() {
+  for (int bps : {2, 4}) {
+    run<0>("PRMT", bps, 256);
+    run<1>("LOP3", bps, 256);
+    run<2>("IMAD", bps, 256);
+    run<3>("IMAD.HI+LOP", bps, 256);
+    run<4>("IADD(x2)", bps, 256);
+    run<5>("VIMNMX3.U16x2", bps, 256);
+    run<6>("VIMNMX.U16x2", bps, 256);
+    run<7>("SHF", bps, 256);
+    run<8>("FFMA", bps, 256);
+    run<9>("LOP3+IMAD", bps, 256);
+    run<10>("LOP3+IMAD+PRMT", bps, 256);
+  }
+  return 0;
+}
