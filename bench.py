@@ -141,6 +141,7 @@ def run_ours(args):
     import synth
     from synth import manifest, torch_dev
     from paper_2503_12964_b200 import Ctx
+    from paper_2503_12964_b200 import dist as cdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -166,18 +167,14 @@ def run_ours(args):
 
     stream = torch.cuda.Stream(device=dev)
     ctx = Ctx(device=local, stream=stream, timing=True)
-    cap = 2 * (v.n // 8 + 1) + 8
-    gbuf = torch.zeros(cap, dtype=torch.int32, device=dev)
-    gathered = torch.zeros(cap * world, dtype=torch.int32, device=dev) if world > 1 else None
+    cap = cdist.capacity_ints([v.n], 8)
+    gathered = [None]
 
     def step():
         with torch.cuda.stream(stream):
             res = ctx.run_videos(item)[0]
-            if world > 1:
-                packed = np.concatenate([[res.detected.size, res.final.size], res.detected,
-                                         res.final]).astype(np.int32)
-                gbuf[:packed.size].copy_(torch.from_numpy(packed), non_blocking=False)
-                dist.all_gather_into_tensor(gathered, gbuf)
+            if world > 1:  # the one collective: all cut lists to every rank (ncclAllGather)
+                gathered[0] = cdist.gather_results([res], cap, device=dev)
         return res
 
     for _ in range(args.warmup):
@@ -213,6 +210,10 @@ def run_ours(args):
     if rank == 0 and not args.frames and os.path.exists(gpath):
         g = json.load(open(gpath))["videos"][0]
         parity = (res.detected.tolist() == g["detected"] and res.final.tolist() == g["final"])
+        if world > 1 and gathered[0] is not None:
+            g0 = [d for d in gathered[0] if d["id"] == 0][0]
+            parity = parity and g0["detected"].tolist() == g["detected"] and g0["final"].tolist() == g["final"] \
+                and len(gathered[0]) == world
 
     # ---- e2e: host (pinned) frames through the same C ABI call, copies inside the timed region
     e2e = None
@@ -320,6 +321,132 @@ def run_ours(args):
     return 0
 
 
+# ---------------------------------------------------------------- batch configs (C3/C4/C5)
+def run_config(args):
+    """--config C3|C4|C5: the config's videos LPT-sharded by whole video over the
+    ranks (strong scaling: the batch is fixed).  A rank whose share fits in HBM
+    keeps it resident and is timed with CUDA events around whole steps; a rank
+    whose share does not fit streams frames through clip_run_videos' fill
+    callback (device generator) and is timed by the library's per-kernel CUDA
+    events (K1+K2+K3; generation excluded) — the JSON says which."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from synth import manifest, torch_dev
+    from paper_2503_12964_b200 import Ctx
+    from paper_2503_12964_b200 import dist as cdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    synth.build(device=True)
+    vids = manifest.config_videos(args.config)
+    if args.max_videos:
+        vids = vids[:args.max_videos]
+    assign = cdist.lpt_assign([v.n * v.W * v.H for v in vids], world)
+    mine = [vids[i] for i in assign[rank]]
+    my_bytes = sum(v.n * v.frame_bytes for v in mine)
+    resident = my_bytes <= args.resident_gb * 1e9
+    tables = [torch_dev.frame_table(v, dev) for v in mine]
+    items = []
+    for v, t in zip(mine, tables):
+        e = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+        torch_dev.gen_emb(v, t, e)
+        f = None
+        if resident:
+            f = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+            torch_dev.gen_frames(v, t, f)
+        items.append({"n": v.n, "H": v.H, "W": v.W, "frames": f, "emb": e, "id": v.id})
+    torch.cuda.synchronize()
+
+    def fill(vi, t0, n, dst, stream):
+        v = mine[vi]
+        return synth.dev_lib().synth_dev_gen_frames(v.seed, v.id, v.W, v.H, t0, n,
+                                                    tables[vi].data_ptr(), dst, stream)
+
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Ctx(device=local, stream=stream, timing=True)
+    cap = cdist.capacity_ints([v.n for v in vids], 8)
+    out = [None, None]
+
+    def step():
+        with torch.cuda.stream(stream):
+            res = ctx.run_videos(items, fill=None if resident else fill) if items else []
+            out[0] = res
+            if world > 1:
+                out[1] = cdist.gather_results(res, cap, device=dev)
+            else:
+                out[1] = [{"id": r.id, "detected": r.detected, "final": r.final} for r in res]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.stats(reset=True)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    st = ctx.stats(reset=True)
+    ms = e0.elapsed_time(e1) / args.steps if resident else (st["k1_ms"] + st["k2_ms"] + st["k3_ms"]) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        flags = torch.tensor([int(resident)], dtype=torch.int32, device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        all_resident = bool(flags.item())
+    else:
+        all_resident = resident
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    total_frames = sum(v.n for v in vids)
+    total_bytes = sum(v.n * v.frame_bytes for v in vids)
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config.upper()}.json")
+    if os.path.exists(gpath) and out[1] is not None:
+        gold = {g["id"]: g for g in json.load(open(gpath))["videos"]}
+        got = {d["id"]: d for d in out[1]}
+        parity = len(got) == len(vids) and all(
+            list(got[v.id]["detected"]) == gold[v.id]["detected"] and list(got[v.id]["final"]) == gold[v.id]["final"]
+            for v in vids)
+    peak, peak_src = _peaks()
+    k1_alg = sum(v.n * (v.frame_bytes + HIST_BYTES) for v in mine)
+    line = {
+        "metric": METRIC, "value": round(total_frames / (ms * 1e-3), 3), "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config.upper()} (BASELINE.json configs)", "videos": len(vids),
+                   "frames": total_frames, "frame_bytes": total_bytes,
+                   "parallelism": f"LPT whole-video sharding over {world} GPU(s), one NCCL all-gather",
+                   "timing": "CUDA events around whole steps (frames resident)" if all_resident else
+                             "library CUDA events around K1+K2+K3 (frames streamed through the device "
+                             "generator callback; generation excluded) on at least one rank"},
+        "hbm_gbs": round(total_bytes / (ms * 1e-3) / 1e9, 1),
+        "frac_of_measured_hbm": round(total_bytes / (ms * 1e-3) / 1e9 / peak, 4),
+        "roofline": {"bound": "hbm", "achieved": round(k1_alg / (st["k1_ms"] / args.steps * 1e-3) / 1e9, 1),
+                     "peak": peak, "unit": "GB/s", "kernel": "k1_hist_kernel (rank 0)",
+                     "frac": round(k1_alg / (st["k1_ms"] / args.steps * 1e-3) / 1e9 / peak, 4)},
+        "gpu_launches": int(st["launches"]), "clocks": clk.summary(), "parity_vs_golden": parity,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -332,9 +459,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="", help="C3|C4|C5: strong-scaling batch run")
+    ap.add_argument("--max-videos", type=int, default=0)
+    ap.add_argument("--resident-gb", type=float, default=150.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config:
+        return run_config(args)
     return run_ours(args)
 
 

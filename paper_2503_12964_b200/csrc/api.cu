@@ -746,7 +746,7 @@ int clip_debug_binmap(clip_ctx* ctx, uint8_t* table) {
   CKS(check_ctx(ctx));
   if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
   CK(k5_binmap_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
-                      k1_mode(ctx->p) == kModeFast, ctx->stream));
+                      k1_mode(ctx->p) == kModeFast, k1_cfg_uses_lut(ctx->k1_cfg), ctx->stream));
   ctx->stats.launches += 1;
   return CLIP_OK;
 }

@@ -109,14 +109,14 @@ constexpr int kCodes = 1 << (16 - kCodeShift);  // 2048
 // pipe on sm_100) to the bit work.
 struct MadK {
   uint32_t one, neg1, neg2, three, four;
-  uint32_t sl8;    // 2^8
-  uint32_t sl24;   // 2^24
+  uint32_t sl4;    // 2^4
+  uint32_t sl20;   // 2^20
   uint32_t sh24;   // 2^24: mulhi(x, sh24) = x >> 8
   uint32_t v3;     // 3 * 2^30: mulhi(x, v3) = (3x) >> 2
   uint32_t sh13;   // 2^13: mulhi(x, sh13) = x >> 19
   uint32_t sl16;   // 2^16: x * sl16 = x << 16
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 4u, 1u << 8, 1u << 24, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 4u, 1u << 4, 1u << 20, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -162,7 +162,7 @@ CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B, MadK k) {
   const uint32_t q3 = cd_mad(d1, k.neg1, cd_mad(num, k.one, 0x01000100u));   // num - d1 + 2^8
   const uint32_t s1 = cd_mad(d, k.three, cd_mad(mx1, k.neg1, 0x10001000u));  // 3d - mx1 + 2^12
   const uint32_t s2 = cd_mad(d, k.three, cd_mad(mx1, k.neg2, 0x20002000u));  // 3d - 2mx1 + 2^13
-  const uint32_t vv = cd_mulhi(mx, k.v3);        // (3 max) >> 2: bits 8,9 of 3 max -> 6,7
+  const uint32_t vv = cd_mad(mx, k.three, 0u) >> 2;  // bits 8,9 of 3 max -> 6,7
   const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
   return (ab & 0x02200220u) | (vv & 0x00C000C0u) | (q3 & 0x01000100u) | (q1 & 0x04000400u) |
          (q2 & 0x08000800u) | (s1 & 0x10001000u) | (s2 & 0x20002000u) | (ris & 0x80008000u);
@@ -170,9 +170,11 @@ CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B, MadK k) {
 
 CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B) { return code_pair(R, G, B, kMadK); }
 
-// Byte offsets (4 * code index) of the two lanes' histogram entries.
-CD_HD uint32_t code_off_lo(uint32_t code, MadK k) { return cd_mulhi(cd_mad(code, k.sl16, 0u), k.sh13); }
-CD_HD uint32_t code_off_hi(uint32_t code, MadK k) { return cd_mulhi(code, k.sh13); }
+// Byte offsets (4 * code index) of the two lanes' histogram entries.  Plain
+// shifts: IMAD.HI runs at a quarter of the IMAD rate on sm_100 (measured,
+// tools/isa_micro.cu), SHF at the ALU rate; lane 0 goes through IMAD (x << 16).
+CD_HD uint32_t code_off_lo(uint32_t code, MadK k) { return cd_mad(code, k.sl16, 0u) >> 19; }
+CD_HD uint32_t code_off_hi(uint32_t code, MadK k) { return code >> 19; }
 
 // code index (lane >> 5) -> bin in [0,162), or 255 for an unreachable code.
 CD_HD uint32_t code_to_bin(uint32_t idx) {
@@ -190,57 +192,65 @@ CD_HD uint32_t code_to_bin(uint32_t idx) {
 // ------------------------------------------------------------ LUT variant
 // The in-sector hue offsets come from a 64 KiB shared-memory table instead of
 // three threshold tests and a select:
-//   lut[d*256 + (na ^ (4d & 0xFC))] = qr | qf << 2,
+//   lut[d*256 + (na ^ d)] = qr | qf << 2,
 //   qr = floor(3 na / d) (rising sectors), qf = floor(3 (d - na) / d) (falling),
-// na = mid - min, d = max - min (0 for grey).  The XOR swizzle spreads equal-na
-// lanes over the 32 banks.  Lane code layout:
-//   bit 5 A, bits 6-7 v, bits 8-9 qr, bits 10-11 qf, bit 12 s1, bit 13 s2,
-//   bit 14 B, bit 15 ris.
+// na = mid - min, d = max - min (entry 0 for grey).  The XOR spreads lanes
+// with equal na over the 32 banks.  Lane code layout (index = lane >> 3):
+//   bit 3 A, bits 4-7 q (qr | qf << 2), bits 8-9 v, bit 10 s1, bit 11 s2,
+//   bit 12 B, bits 13-14 0, bit 15 C   -> 5120 code indices used.
+constexpr int kLutCodeShift = 3;
+constexpr int kLutCodes = 5120;
+
 CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
   if (d == 0) return 0u;
   const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
   return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
 }
-CD_HD uint32_t lut_index(uint32_t na, uint32_t d) { return d * 256u + (na ^ ((4u * d) & 0xFCu)); }
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d) { return d * 256u + (na ^ d); }
 
 // Part 1 (before the table lookups): returns the partial code and the two
-// lanes' table indices.
+// lanes' table indices.  The sector is carried as the three raw ordering
+// flags A, B, C (parity is decoded from them in code_to_bin_lut).
 CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   constexpr uint32_t kB15 = 0x80008000u;
   const uint32_t mx = cd_max3_u16x2(R, G, B);
   const uint32_t mn = cd_min3_u16x2(R, G, B);
   const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, R + G + B));  // mid - min
-  const uint32_t nas = na ^ (cd_mad(d, k.four, 0u) & 0x00FC00FCu);         // swizzle
+  const uint32_t sum = cd_mad(B, k.one, cd_mad(R, k.one, G));
+  const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, sum));  // mid - min
+  const uint32_t nas = na ^ d;                                        // bank swizzle
   i0 = cd_prmt(nas, d, 0x1140u);  // lane 0: nas | d << 8
   i1 = cd_prmt(nas, d, 0x3362u);  // lane 1
   const uint32_t R15 = cd_mad(R, k.one, kB15);
-  const uint32_t tA = cd_mad(G, k.neg1, R15);                     // bit 15: r >= g
-  const uint32_t tB = cd_mad(B, k.neg1, cd_mad(G, k.one, kB15));  // bit 15: g >= b
-  const uint32_t tC = cd_mad(B, k.neg1, R15);                     // bit 15: r >= b
-  const uint32_t ris = tA ^ tB ^ tC;                              // bit 15: rising sector
+  const uint32_t tA = cd_mad(G, k.neg1, R15);  // bit 15: r >= g   (IMAD)
+  const uint32_t tB = G + kB15 - B;            // bit 15: g >= b   (IADD3)
+  const uint32_t tC = cd_mad(B, k.neg1, R15);  // bit 15: r >= b   (IMAD)
   const uint32_t mx1 = cd_max_u16x2(mx, 0x00010001u);
-  const uint32_t z1 = cd_mad(mx1, k.neg1, 0x10001000u);
-  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx1 + 2^12
-  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx1 + 2^13
-  const uint32_t vv = cd_mulhi(mx, k.v3);      // bits 8,9 of 3 max -> 6,7
+  const uint32_t z1 = cd_mad(mx1, k.neg1, 0x04000400u);
+  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx1 + 2^10
+  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx1 + 2^11
+  const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8,9 of 3 max = v
   const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
-  return (ab & 0x40204020u) | (vv & 0x00C000C0u) | (s1 & 0x10001000u) | (s2 & 0x20002000u) |
-         (ris & 0x80008000u);
+  return (ab & 0x10081008u) | (m3 & 0x03000300u) | (s1 & 0x04000400u) | (s2 & 0x08000800u) |
+         (tC & 0x80008000u);
 }
 // Part 2: add the two looked-up entries (q0 for lane 0, q1 for lane 1).
 CD_HD uint32_t code_pair_lut_post(uint32_t pre, uint32_t q0, uint32_t q1, MadK k) {
-  return cd_mad(q1, k.sl24, cd_mad(q0, k.sl8, pre));
+  return cd_mad(q1, k.sl20, cd_mad(q0, k.sl4, pre));
 }
+// Byte offsets (4 * code index) of the two lanes' entries.
+CD_HD uint32_t lut_off_lo(uint32_t code, MadK k) { return cd_mad(code, k.sl16, 0u) >> 17; }
+CD_HD uint32_t lut_off_hi(uint32_t code, MadK k) { return code >> 17; }
 
 CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
-  const uint32_t c = idx << kCodeShift;
-  const uint32_t A = (c >> 5) & 1u, v = (c >> 6) & 3u, qr = (c >> 8) & 3u, qf = (c >> 10) & 3u;
-  const uint32_t s1 = (c >> 12) & 1u, s2 = (c >> 13) & 1u, B = (c >> 14) & 1u, ris = (c >> 15) & 1u;
-  const uint32_t C = A ^ B ^ ris;
+  const uint32_t c = idx << kLutCodeShift;
+  const uint32_t A = (c >> 3) & 1u, qr = (c >> 4) & 3u, qf = (c >> 6) & 3u, v = (c >> 8) & 3u;
+  const uint32_t s1 = (c >> 10) & 1u, s2 = (c >> 11) & 1u, B = (c >> 12) & 1u;
+  const uint32_t z = (c >> 13) & 3u, C = (c >> 15) & 1u;
+  const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
   const uint32_t oidx = (A << 2) | (B << 1) | C;
-  if (oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
+  if (z || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
   const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
   return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
 }
@@ -250,8 +260,8 @@ CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
 CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
                    uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23, MadK k) {
   // w0 = [r0 g0 b0 r1], w1 = [g1 b1 r2 g2], w2 = [b2 r3 g3 b3] (byte 0 first)
-  const uint32_t s0 = cd_mulhi(w0, k.sh24);  // w0 >> 8 = [g0 b0 r1 0]
-  const uint32_t s1 = cd_mulhi(w1, k.sh24);  // w1 >> 8 = [b1 r2 g2 0]
+  const uint32_t s0 = w0 >> 8;  // [g0 b0 r1 0]
+  const uint32_t s1 = w1 >> 8;  // [b1 r2 g2 0]
   R01 = cd_prmt(w0, 0u, 0x4340u);
   G01 = cd_prmt(s0, w1, 0x3430u);
   B01 = cd_prmt(s0, w1, 0x3531u);

@@ -29,7 +29,6 @@ namespace {
 
 constexpr int kStageGroups = 512;  // 48-byte groups per stage (24 KiB), common to all configs
 constexpr int kStageBytes = kStageGroups * 48;
-constexpr int kHistEntries = kCodes;  // 2048 codes (fast) or <= 256 bins (generic)
 constexpr int kLutBytes = 65536;
 
 // Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
@@ -42,28 +41,31 @@ constexpr int kNumCfgs = 7;
 
 template <int STAGES, int LUT>
 struct K1Smem {
+  static constexpr int kEntries = LUT ? kLutCodes : kCodes;
   alignas(128) uint8_t buf[STAGES][kStageBytes];
   uint8_t lut[LUT ? kLutBytes : 16];
-  uint32_t hist[kHistEntries];  // CTA-shared code (or bin) histogram
-  uint32_t binacc[256];         // flush: per-bin sums
-  uint8_t c2b[kCodes];          // code -> bin
+  uint32_t hist[kEntries];  // CTA-shared code (or bin) histogram
+  uint32_t binacc[256];     // flush: per-bin sums
+  uint8_t c2b[kEntries];    // code -> bin
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   MadK mk;
 };
 
+// Walks the flattened (segment, frame, stage) space with 32-bit counters.
 struct StageIter {
   const HistSeg* segs;
-  int32_t seg;
-  int64_t frame, st;
+  int32_t seg, frame, st;
   // cached fields of segs[seg]
-  int64_t groups, stages, n_frames;
+  int32_t stages, last_ng, n_frames;
+  int64_t groups;
   const uint8_t* frames;
   __device__ void load() {
     const HistSeg& g = segs[seg];
     groups = g.groups;
-    stages = g.stages;
-    n_frames = g.n_frames;
+    stages = (int32_t)g.stages;
+    n_frames = (int32_t)g.n_frames;
+    last_ng = (int32_t)(g.groups - (g.stages - 1) * kStageGroups);
     frames = g.frames;
   }
   __device__ void seek(const HistSeg* s, int32_t nseg, int64_t g) {
@@ -75,12 +77,13 @@ struct StageIter {
     }
     seg = lo;
     load();
-    int64_t rel = g - s[lo].stage_base;
-    frame = rel / stages;
-    st = rel - frame * stages;
+    const int64_t rel = g - s[lo].stage_base;
+    frame = (int32_t)(rel / stages);
+    st = (int32_t)(rel - (int64_t)frame * stages);
   }
+  __device__ __forceinline__ int32_t ng() const { return st == stages - 1 ? last_ng : kStageGroups; }
   // advance; returns true if the frame (or segment) changed
-  __device__ bool next(bool more) {
+  __device__ __forceinline__ bool next(bool more) {
     if (++st == stages) {
       st = 0;
       if (++frame == n_frames) {
@@ -113,12 +116,11 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, co
   const uint4* p = reinterpret_cast<const uint4*>(src);
   const uint4 a = p[0], b = p[1], c = p[2];
   const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-  if (MODE == kModeRead) {
+  if constexpr (MODE == kModeRead) {
 #pragma unroll
     for (int i = 0; i < 12; ++i) xacc ^= w[i];
     return;
-  }
-  if (MODE == kModeFast) {
+  } else if constexpr (MODE == kModeFast) {
     char* hb = reinterpret_cast<char*>(hist);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -135,21 +137,28 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, co
         c01 = code_pair(R01, G01, B01, mk);
         c23 = code_pair(R23, G23, B23, mk);
       }
-      // byte offsets of the code-histogram entries: 4 * (lane >> 5)
-      hist_inc(hb, code_off_lo(c01, mk));
-      hist_inc(hb, code_off_hi(c01, mk));
-      hist_inc(hb, code_off_lo(c23, mk));
-      hist_inc(hb, code_off_hi(c23, mk));
+      // byte offsets of the code-histogram entries
+      if (LUT) {
+        hist_inc(hb, lut_off_lo(c01, mk));
+        hist_inc(hb, lut_off_hi(c01, mk));
+        hist_inc(hb, lut_off_lo(c23, mk));
+        hist_inc(hb, lut_off_hi(c23, mk));
+      } else {
+        hist_inc(hb, code_off_lo(c01, mk));
+        hist_inc(hb, code_off_hi(c01, mk));
+        hist_inc(hb, code_off_lo(c23, mk));
+        hist_inc(hb, code_off_hi(c23, mk));
+      }
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int o = 3 * i;
-    const uint32_t r = __byte_perm(w[o >> 2], 0u, 0x4440u | (o & 3));
-    const uint32_t g = __byte_perm(w[(o + 1) >> 2], 0u, 0x4440u | ((o + 1) & 3));
-    const uint32_t bb = __byte_perm(w[(o + 2) >> 2], 0u, 0x4440u | ((o + 2) & 3));
-    atomicAdd(&hist[bin_generic(r, g, bb, nh, ns, nv)], 1u);
+    for (int i = 0; i < 16; ++i) {
+      const int o = 3 * i;
+      const uint32_t r = __byte_perm(w[o >> 2], 0u, 0x4440u | (o & 3));
+      const uint32_t g = __byte_perm(w[(o + 1) >> 2], 0u, 0x4440u | ((o + 1) & 3));
+      const uint32_t bb = __byte_perm(w[(o + 2) >> 2], 0u, 0x4440u | ((o + 2) & 3));
+      atomicAdd(&hist[bin_generic(r, g, bb, nh, ns, nv)], 1u);
+    }
   }
 }
 
@@ -171,16 +180,16 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
 
-  const uint32_t nentries = MODE == kModeFast ? (uint32_t)kCodes : nbins;
-  for (int i = tid; i < kHistEntries; i += kThreads) sm.hist[i] = 0u;
+  constexpr int kEntries = K1Smem<STAGES, LUT>::kEntries;
+  const uint32_t nentries = MODE == kModeFast ? (uint32_t)kEntries : nbins;
+  for (int i = tid; i < kEntries; i += kThreads) sm.hist[i] = 0u;
   for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
   if (MODE == kModeFast)
-    for (int i = tid; i < kCodes; i += kThreads)
+    for (int i = tid; i < kEntries; i += kThreads)
       sm.c2b[i] = (uint8_t)(kUseLut ? code_to_bin_lut(i) : code_to_bin(i));
   if (kUseLut)
     for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8, nas = (uint32_t)i & 255u;
-      const uint32_t na = nas ^ ((4u * d) & 0xFCu);
+      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ d;
       sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
   if (tid == 0) {
@@ -200,17 +209,19 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const uint64_t pol = policy_evict_first();
       StageIter it;
       it.seek(segs, nseg, s_begin);
-      uint32_t i = 0;
-      for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-        const uint32_t slot = i % STAGES, par = (i / STAGES) & 1u;
+      const int32_t n = (int32_t)(s_end - s_begin);
+      uint32_t slot = 0, par = 0;
+      for (int32_t i = 0; i < n; ++i) {
         if (i >= STAGES) mbar_wait(&sm.empty[slot], par ^ 1u);
-        const int64_t g0 = it.st * kStageGroups;
-        const int64_t ng = min((int64_t)kStageGroups, it.groups - g0);
-        const uint32_t bytes = (uint32_t)(ng * 48);
-        const uint8_t* src = it.frames + (it.frame * it.groups + g0) * 48;
+        const uint32_t bytes = (uint32_t)it.ng() * 48u;
+        const uint8_t* src = it.frames + ((int64_t)it.frame * it.groups + (int64_t)it.st * kStageGroups) * 48;
         mbar_arrive_expect_tx(&sm.full[slot], bytes);
         bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
-        it.next(s + 1 < s_end);
+        it.next(i + 1 < n);
+        if (++slot == STAGES) {
+          slot = 0;
+          par ^= 1u;
+        }
       }
     }
     return;
@@ -229,11 +240,10 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   uint32_t xacc = 0;
   StageIter it;
   it.seek(segs, nseg, s_begin);
-  uint32_t i = 0;
-  for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-    const uint32_t slot = i % STAGES, par = (i / STAGES) & 1u;
-    const int64_t g0 = it.st * kStageGroups;
-    const int ng = (int)min((int64_t)kStageGroups, it.groups - g0);
+  const int32_t n = (int32_t)(s_end - s_begin);
+  uint32_t slot = 0, par = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const int ng = it.ng();
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
 #pragma unroll
@@ -243,10 +253,13 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    if (++slot == STAGES) {
+      slot = 0;
+      par ^= 1u;
+    }
 
-    const int32_t seg_now = it.seg;
-    const int64_t frame_now = it.frame;
-    const bool last = (s + 1 == s_end);
+    const int32_t seg_now = it.seg, frame_now = it.frame;
+    const bool last = (i + 1 == n);
     const bool changed = it.next(!last);
     if (MODE != kModeRead && (last || changed)) {
       // flush the frame's partial histogram
@@ -259,7 +272,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
         }
       }
       named_bar_sync(1, kConsumers);
-      uint32_t* gh = segs[seg_now].hist + frame_now * nbins;
+      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
       for (uint32_t bn = tid; bn < nbins; bn += kConsumers) {
         const uint32_t sum = sm.binacc[bn];
         if (sum) {
@@ -353,30 +366,61 @@ cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
 }
 
 // ---------------------------------------------------------------- K5 (test)
+// The hot-path bin evaluation over all 2^24 colours: colour c in lane 0 and
+// colour c ^ 0xA5A5A5 in lane 1 of the two-pixel code, through the same code
+// -> bin tables (and, for the LUT variant, the same shared-memory hue table)
+// as K1.  out[0][c] = lane-0 result, out[1][c] = lane-1 result.
 namespace {
-__global__ void k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv,
-                                 int fast) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (1u << 24)) return;
-  const uint32_t r = c >> 16, g = (c >> 8) & 255u, b = c & 255u;
-  if (!fast) {
-    out[c] = out[c + (1u << 24)] = (uint8_t)bin_generic(r, g, b, nh, ns, nv);
-    return;
+template <int LUT>
+__global__ void __launch_bounds__(256)
+k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
+                 MadK mk) {
+  extern __shared__ __align__(16) uint8_t lut[];
+  if (LUT) {
+    for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) {
+      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ d;
+      lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+    }
+    __syncthreads();
   }
-  // the hot-path pair code, this colour in lane 0 and colour c ^ 0xA5A5A5 in lane 1
-  const uint32_t c2 = c ^ 0xA5A5A5u;
-  const uint32_t code = code_pair(r | ((c2 >> 16) << 16), g | (((c2 >> 8) & 255u) << 16),
-                                  b | ((c2 & 255u) << 16));
-  const uint32_t b0 = code_to_bin((code & 0xFFFFu) >> kCodeShift);
-  const uint32_t b1 = code_to_bin(code >> (16 + kCodeShift));
-  out[c] = (uint8_t)b0;                  // table 0: lane 0
-  out[(1u << 24) + c2] = (uint8_t)b1;    // table 1: lane 1
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (1u << 24);
+       c += gridDim.x * blockDim.x) {
+    const uint32_t r = c >> 16, g = (c >> 8) & 255u, b = c & 255u;
+    if (!fast) {
+      out[c] = out[c + (1u << 24)] = (uint8_t)bin_generic(r, g, b, nh, ns, nv);
+      continue;
+    }
+    const uint32_t c2 = c ^ 0xA5A5A5u;
+    const uint32_t R = r | ((c2 >> 16) << 16), G = g | (((c2 >> 8) & 255u) << 16),
+                   B = b | ((c2 & 255u) << 16);
+    uint32_t b0, b1;
+    if (LUT) {
+      uint32_t i0, i1;
+      const uint32_t pre = code_pair_lut_pre(R, G, B, mk, i0, i1);
+      const uint32_t code = code_pair_lut_post(pre, lut[i0], lut[i1], mk);
+      b0 = code_to_bin_lut(lut_off_lo(code, mk) >> 2);
+      b1 = code_to_bin_lut(lut_off_hi(code, mk) >> 2);
+    } else {
+      const uint32_t code = code_pair(R, G, B, mk);
+      b0 = code_to_bin(code_off_lo(code, mk) >> 2);
+      b1 = code_to_bin(code_off_hi(code, mk) >> 2);
+    }
+    out[c] = (uint8_t)b0;                // table 0: lane 0
+    out[(1u << 24) + c2] = (uint8_t)b1;  // table 1: lane 1
+  }
 }
 }  // namespace
 
+int k1_cfg_uses_lut(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].lut : 0; }
+
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                             cudaStream_t stream) {
-  k5_binmap_kernel<<<(1u << 24) / 256, 256, 0, stream>>>(out, nh, ns, nv, fast);
+                             int lut, cudaStream_t stream) {
+  if (fast && lut) {
+    cudaFuncSetAttribute(k5_binmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
+    k5_binmap_kernel<1><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
+  } else {
+    k5_binmap_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, fast, kMadK);
+  }
   return cudaGetLastError();
 }
 

@@ -18,8 +18,9 @@ int k1_grid(int cfg, int sm_count, int64_t total_stages);
 cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
                       int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
                       uint32_t* sink, int grid, cudaStream_t stream);
+int k1_cfg_uses_lut(int cfg);
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                             cudaStream_t stream);
+                             int lut, cudaStream_t stream);
 
 // ---- K2 (cuts.cu)
 struct VideoDesc {

@@ -29,14 +29,18 @@ int main(int argc, char** argv) {
     const uint32_t G = ((c >> 8) & 255u) | (((c2 >> 8) & 255u) << 16);
     const uint32_t B = (c & 255u) | ((c2 & 255u) << 16);
     const uint32_t code = code_pair(R, G, B);
-    t0[c] = (uint8_t)code_to_bin((code & 0xFFFFu) >> kCodeShift);
-    t1[c2] = (uint8_t)code_to_bin(code >> (16 + kCodeShift));
+    t0[c] = (uint8_t)code_to_bin(code_off_lo(code, kMadK) >> 2);
+    t1[c2] = (uint8_t)code_to_bin(code_off_hi(code, kMadK) >> 2);
     tg[c] = (uint8_t)bin_generic(c >> 16, (c >> 8) & 255u, c & 255u, nh, ns, nv);
     uint32_t i0, i1;
     const uint32_t pre = code_pair_lut_pre(R, G, B, kMadK, i0, i1);
     const uint32_t lc = code_pair_lut_post(pre, lut[i0], lut[i1], kMadK);
-    l0[c] = (uint8_t)code_to_bin_lut((lc & 0xFFFFu) >> kCodeShift);
-    l1[c2] = (uint8_t)code_to_bin_lut(lc >> (16 + kCodeShift));
+    l0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
+    l1[c2] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);
+    if (lut_off_lo(lc, kMadK) >= 4u * kLutCodes || lut_off_hi(lc, kMadK) >= 4u * kLutCodes) {
+      fprintf(stderr, "lut code offset out of range\n");
+      return 1;
+    }
   }
   // unpack4 on pseudo-random bytes
   uint32_t x = 12345u;

@@ -40,6 +40,31 @@ __device__ __forceinline__ uint32_t shf(uint32_t a, uint32_t b, uint32_t c) {
   asm volatile("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
 }
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t imad_imm(uint32_t a, uint32_t c) {
+  uint32_t r;
+  asm volatile("mad.lo.u32 %0, %1, 3, %2;" : "=r"(r) : "r"(a), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t iadd3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm volatile("{ .reg .u32 t; add.u32 t, %1, %2; sub.u32 %0, t, %3; }" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 __device__ __forceinline__ float ffma(float a, float b, float c) {
   float r;
   asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -70,6 +95,13 @@ __global__ void bench(uint32_t* out, int iters, uint32_t k1, uint32_t k2, long l
       if (OP == 9) {  // mixed: half ALU (lop3), half FMA (mad)
         if (i & 1) x[i] = lop3(x[i], k1, k2); else x[i] = mad(x[i], k1, k2);
       }
+      if (OP == 11) x[i] = hfma2(x[i], k1 | 0x3C003C00u, k2);
+      if (OP == 12) x[i] = hadd2(x[i], k1);
+      if (OP == 13) x[i] = hmax2(x[i], k1 + (uint32_t)i) ^ k2;
+      if (OP == 14) x[i] = imad_imm(x[i], k2 + (uint32_t)i);
+      if (OP == 15) x[i] = iadd3(x[i], k1, k2 + (uint32_t)i);
+      if (OP == 16) x[i] = vmax2(x[i], k1 + (uint32_t)i) ^ k2;
+      if (OP == 17) x[i] = mulhi(x[i], k1 + (uint32_t)i);
       if (OP == 10) {  // mixed: 1/3 lop3, 1/3 mad, 1/3 prmt
         if (i % 3 == 0) x[i] = lop3(x[i], k1, k2);
         else if (i % 3 == 1) x[i] = mad(x[i], k1, k2);
@@ -107,7 +139,7 @@ void run(const char* name, int blocks_per_sm, int threads) {
   long long c;
   cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
   const double warp_instr = (double)sms * blocks_per_sm * (threads / 32) * iters * 8.0;
-  const double per_sm_per_clk = warp_instr / sms / (double)c;
+  const double per_sm_per_clk = warp_instr / sms / ((double)ms * 1e-3 * 1.92e9);
   printf("{\"op\": \"%s\", \"warps_per_sm\": %d, \"cycles\": %lld, \"ms\": %.3f, \"warp_instr_per_clk_per_sm\": %.3f}\n",
          name, blocks_per_sm * threads / 32, c, ms, per_sm_per_clk);
   cudaFree(out);
@@ -115,7 +147,7 @@ void run(const char* name, int blocks_per_sm, int threads) {
 }
 
 int main() {
-  for (int bps : {2, 4}) {
+  for (int bps : {4}) {
     run<0>("PRMT", bps, 256);
     run<1>("LOP3", bps, 256);
     run<2>("IMAD", bps, 256);
@@ -127,6 +159,13 @@ int main() {
     run<8>("FFMA", bps, 256);
     run<9>("LOP3+IMAD", bps, 256);
     run<10>("LOP3+IMAD+PRMT", bps, 256);
+    run<11>("HFMA2", bps, 256);
+    run<12>("HADD2", bps, 256);
+    run<13>("HMNMX2+LOP3", bps, 256);
+    run<14>("IMAD-imm", bps, 256);
+    run<15>("IADD3-3op", bps, 256);
+    run<16>("VIMNMX.U16x2+LOP3", bps, 256);
+    run<17>("IMAD.HI", bps, 256);
   }
   return 0;
 }
