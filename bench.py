@@ -39,31 +39,67 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event (throttle) reasons sampled every ~20 ms through
+    NVML (nvidia-smi fallback) during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown"}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.02):
         self.index = index
-        self.rows = []
+        self.period = period
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            self.mx.append(mx)
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+            self._stop.wait(self.period)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
-                out = subprocess.check_output(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"], text=True, timeout=5)
-                self.rows.append([x.strip() for x in out.strip().split(",")])
+                out = subprocess.check_output(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                               "--format=csv,noheader,nounits"], text=True, timeout=5)
+                r = [x.strip() for x in out.strip().split(",")]
+                self.sm.append(float(r[0]))
+                self.mx.append(float(r[1]))
+                for i, n in enumerate(names):
+                    if r[2 + i].lower().startswith("active"):
+                        self.reasons.add(n)
             except Exception:
                 pass
             self._stop.wait(0.2)
 
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            try:
+                self._run_nvml(nv)
+            finally:
+                nv.nvmlShutdown()
+        except Exception:
+            self._run_smi()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
@@ -71,16 +107,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 # ---------------------------------------------------------------- CPU oracle leg
@@ -169,12 +199,16 @@ def run_ours(args):
     ctx = Ctx(device=local, stream=stream, timing=True)
     cap = cdist.capacity_ints([v.n], 8)
     gathered = [None]
+    gather_wall = [0.0]
 
     def step():
         with torch.cuda.stream(stream):
             res = ctx.run_videos(item)[0]
-            if world > 1:  # the one collective: all cut lists to every rank (ncclAllGather)
+            if world > 1 and not args.no_gather:
+                # the one collective: all cut lists to every rank (ncclAllGather)
+                t0 = time.perf_counter()
                 gathered[0] = cdist.gather_results([res], cap, device=dev)
+                gather_wall[0] += time.perf_counter() - t0
         return res
 
     for _ in range(args.warmup):
@@ -196,10 +230,14 @@ def run_ours(args):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     st = ctx.stats(reset=True)
+    per_rank_ms = [ms / args.steps]
+    gather_ms = 1000.0 * gather_wall[0] / max(1, args.steps + args.warmup)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+        allt = torch.empty(world, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(allt, t)
+        per_rank_ms = [x / args.steps for x in allt.cpu().tolist()]
+        ms_max = max(allt.cpu().tolist())
     else:
         ms_max = ms
     ms_step = ms_max / args.steps
@@ -310,6 +348,8 @@ def run_ours(args):
                                "k2": round(st["k2_ms"] / args.steps, 4),
                                "k3": round(st["k3_ms"] / args.steps, 4)},
         "gpu_launches": int(st["launches"]),
+        "per_rank_ms_per_step": [round(x, 4) for x in per_rank_ms],
+        "gather_wall_ms_per_step_rank0": round(gather_ms, 4) if world > 1 else None,
         "clocks": clk.summary(),
         "parity_vs_golden": parity,
         "cpu_baseline": cpu,
@@ -450,7 +490,7 @@ def run_config(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=0, help="debug: truncate the C2 video")
@@ -459,6 +499,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gather", action="store_true", help="diagnosis: skip the result all-gather")
     ap.add_argument("--config", default="", help="C3|C4|C5: strong-scaling batch run")
     ap.add_argument("--max-videos", type=int, default=0)
     ap.add_argument("--resident-gb", type=float, default=150.0)

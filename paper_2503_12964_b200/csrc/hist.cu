@@ -32,12 +32,17 @@ constexpr int kStageBytes = kStageGroups * 48;
 constexpr int kLutBytes = 65536;
 
 // Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
+// quad = lane-contiguous layout: each lane takes 4 pixels (12 bytes, three
+// conflict-free LDS.32) so one warp instruction covers 128 adjacent pixels
+// (better same-address aggregation of the histogram atomics and of the hue
+// table lookups on spatially coherent content).
 struct K1Cfg {
-  int stages, ctas_per_sm, warps, lut;
+  int stages, ctas_per_sm, warps, lut, quad;
 };
-constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0}, {2, 3, 8, 0}, {3, 2, 8, 0}, {6, 1, 8, 0},
-                           {4, 1, 16, 1}, {2, 1, 16, 1}, {4, 1, 16, 0}};
-constexpr int kNumCfgs = 7;
+constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
+                           {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
+                           {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}};
+constexpr int kNumCfgs = 9;
 
 template <int STAGES, int LUT>
 struct K1Smem {
@@ -162,7 +167,36 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, co
   }
 }
 
-template <int MODE, int STAGES, int MINB, int CW, int LUT>
+// 4 pixels (12 bytes at a 4-byte aligned smem address) -> 4 histogram increments
+template <int LUT>
+__device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, const uint8_t* lut,
+                                         MadK mk) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(src);
+  const uint32_t w0 = p[0], w1 = p[1], w2 = p[2];
+  char* hb = reinterpret_cast<char*>(hist);
+  uint32_t R01, G01, B01, R23, G23, B23;
+  unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
+  if constexpr (LUT) {
+    uint32_t a0, a1, b0, b1;
+    const uint32_t p01 = code_pair_lut_pre(R01, G01, B01, mk, a0, a1);
+    const uint32_t p23 = code_pair_lut_pre(R23, G23, B23, mk, b0, b1);
+    const uint32_t c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
+    const uint32_t c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
+    hist_inc(hb, lut_off_lo(c01, mk));
+    hist_inc(hb, lut_off_hi(c01, mk));
+    hist_inc(hb, lut_off_lo(c23, mk));
+    hist_inc(hb, lut_off_hi(c23, mk));
+  } else {
+    const uint32_t c01 = code_pair(R01, G01, B01, mk);
+    const uint32_t c23 = code_pair(R23, G23, B23, mk);
+    hist_inc(hb, code_off_lo(c01, mk));
+    hist_inc(hb, code_off_hi(c01, mk));
+    hist_inc(hb, code_off_lo(c23, mk));
+    hist_inc(hb, code_off_hi(c23, mk));
+  }
+}
+
+template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD>
 __global__ void __launch_bounds__(CW * 32 + 32, MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
@@ -246,10 +280,16 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const int ng = it.ng();
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
+    if constexpr (QUAD && MODE == kModeFast) {
+      const int nq = ng * 4;
+#pragma unroll 2
+      for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kGPT; ++j) {
-      const int gi = tid + j * kConsumers;
-      if (gi < ng) bin_group<MODE, LUT>(buf + gi * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
+      for (int j = 0; j < kGPT; ++j) {
+        const int gi = tid + j * kConsumers;
+        if (gi < ng) bin_group<MODE, LUT>(buf + gi * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -289,8 +329,8 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 template <int MODE, int C>
 struct Cfg {
   static constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm, W = kCfgs[C].warps,
-                       L = kCfgs[C].lut;
-  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L>; }
+                       L = kCfgs[C].lut, Q = kCfgs[C].quad;
+  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q>; }
   static constexpr size_t smem() { return sizeof(K1Smem<S, L>); }
 };
 
@@ -310,7 +350,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
 #define K1_CASE(c) \
   case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   switch (cfg) {
-    K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6)
+    K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -332,7 +372,9 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 3>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 4>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 5>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 6>();
+  if ((e = configure_cfg<MODE, 6>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 7>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 8>();
 }
 
 }  // namespace

@@ -42,6 +42,7 @@ def main():
     os.environ.pop("CLIPDETECT_K1_CFG", None)
     out = {}
     for name, v in [("c2", manifest.subsample(manifest.c2_video(0), n)),
+                    ("c2v1", manifest.subsample(manifest.c2_video(1), n)),
                     ("noise", manifest.noise_video(0, 1280, 720, n))]:
         table = torch_dev.frame_table(v, dev)
         frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
