@@ -108,15 +108,12 @@ constexpr int kCodes = 1 << (16 - kCodeShift);  // 2048
 // the FMA pipe and leaves the ALU pipe (LOP3/PRMT/VIMNMX/SHF, the binding
 // pipe on sm_100) to the bit work.
 struct MadK {
-  uint32_t one, neg1, neg2, three, four;
-  uint32_t sl4;    // 2^4
-  uint32_t sl20;   // 2^20
-  uint32_t sh24;   // 2^24: mulhi(x, sh24) = x >> 8
-  uint32_t v3;     // 3 * 2^30: mulhi(x, v3) = (3x) >> 2
-  uint32_t sh13;   // 2^13: mulhi(x, sh13) = x >> 19
-  uint32_t sl16;   // 2^16: x * sl16 = x << 16
+  uint32_t one, neg1, neg2, three;
+  uint32_t sl4;   // 2^4
+  uint32_t sl16;  // 2^16
+  uint32_t sl20;  // 2^20
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 4u, 1u << 4, 1u << 20, 1u << 24, 0xC0000000u, 1u << 13, 1u << 16};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -128,15 +125,6 @@ CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #endif
 }
 
-CD_HD uint32_t cd_mulhi(uint32_t a, uint32_t b) {
-#if defined(__CUDA_ARCH__)
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-#else
-  return (uint32_t)(((uint64_t)a * b) >> 32);
-#endif
-}
 
 // Two pixels: R, G, B hold (channel of pixel 0) | (channel of pixel 1) << 16.
 // Every lane result below stays in [0, 2^16): no borrow or carry crosses lanes.

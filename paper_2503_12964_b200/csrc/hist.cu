@@ -41,8 +41,9 @@ struct K1Cfg {
 };
 constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
                            {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
-                           {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}};
-constexpr int kNumCfgs = 9;
+                           {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
+                           {4, 2, 8, 0, 2}};
+constexpr int kNumCfgs = 12;
 
 template <int STAGES, int LUT>
 struct K1Smem {
@@ -280,10 +281,20 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const int ng = it.ng();
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
-    if constexpr (QUAD && MODE == kModeFast) {
+    if constexpr (QUAD == 1 && MODE == kModeFast) {
       const int nq = ng * 4;
 #pragma unroll 2
       for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+    } else if constexpr (QUAD == 2 && MODE == kModeFast) {
+      // all of a lane's quads of a full stage issued together (more independent work per warp)
+      constexpr int kQPL = 4 * kStageGroups / kConsumers;
+      const int nq = ng * 4;
+      if (nq == kQPL * kConsumers) {
+#pragma unroll
+        for (int j = 0; j < kQPL; ++j) bin_quad<LUT>(buf + (tid + j * kConsumers) * 12, wh, sm.lut, mk);
+      } else {
+        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < kGPT; ++j) {
@@ -351,6 +362,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
+    K1_CASE(9) K1_CASE(10) K1_CASE(11)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -374,7 +386,10 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 5>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 6>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 7>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 8>();
+  if ((e = configure_cfg<MODE, 8>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 9>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 10>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 11>();
 }
 
 }  // namespace
