@@ -36,14 +36,16 @@ constexpr int kLutBytes = 65536;
 // conflict-free LDS.32) so one warp instruction covers 128 adjacent pixels
 // (better same-address aggregation of the histogram atomics and of the hue
 // table lookups on spatially coherent content).
+// noprod = no dedicated producer warp: the last consumer warp to release a
+// ring slot issues the slot's next TMA copy (lets a CTA hold 32 consumer warps).
 struct K1Cfg {
-  int stages, ctas_per_sm, warps, lut, quad;
+  int stages, ctas_per_sm, warps, lut, quad, noprod = 0;
 };
 constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
                            {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
                            {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
-                           {4, 2, 8, 0, 2}};
-constexpr int kNumCfgs = 12;
+                           {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1}};
+constexpr int kNumCfgs = 14;
 
 template <int STAGES, int LUT>
 struct K1Smem {
@@ -55,6 +57,7 @@ struct K1Smem {
   uint8_t c2b[kEntries];    // code -> bin
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
+  uint32_t cnt[STAGES];  // noprod: warps done with the slot's current stage
   MadK mk;
 };
 
@@ -197,14 +200,14 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   }
 }
 
-template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD>
-__global__ void __launch_bounds__(CW * 32 + 32, MINB)
+template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD>
+__global__ void __launch_bounds__(CW * 32 + (NOPROD ? 0 : 32), MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
   constexpr int kConsumers = CW * 32;
-  constexpr int kThreads = kConsumers + 32;
-  constexpr int kGPT = kStageGroups / kConsumers;
-  static_assert(kGPT * kConsumers == kStageGroups, "stage must split evenly");
+  constexpr int kThreads = kConsumers + (NOPROD ? 0 : 32);
+  constexpr int kGPT = kStageGroups / kConsumers;  // 0 when a stage has fewer groups than lanes
+  static_assert(kGPT == 0 || kGPT * kConsumers == kStageGroups, "stage must split evenly");
   constexpr bool kUseLut = (MODE == kModeFast) && LUT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   K1Smem<STAGES, LUT>& sm = *reinterpret_cast<K1Smem<STAGES, LUT>*>(smem_raw);
@@ -232,13 +235,33 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], CW);
+      sm.cnt[i] = 0u;
     }
     fence_mbar_init();
   }
   __syncthreads();
   if (s_begin >= s_end) return;
 
-  if (warp == CW) {
+  // noprod: the first STAGES copies come from thread 0; `ahead` tracks the stage
+  // a slot is refilled with (i + STAGES) in every warp
+  StageIter ahead;
+  uint64_t pol = 0;
+  if constexpr (NOPROD) {
+    pol = policy_evict_first();
+    const int32_t n = (int32_t)(s_end - s_begin);
+    ahead.seek(segs, nseg, s_begin);
+    for (int32_t i = 0; i < STAGES && i < n; ++i) {
+      if (tid == 0) {
+        const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
+        const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * kStageGroups) * 48;
+        mbar_arrive_expect_tx(&sm.full[i], bytes);
+        bulk_g2s(sm.buf[i], src, bytes, &sm.full[i], pol);
+      }
+      ahead.next(i + 1 < n);
+    }
+  }
+
+  if (!NOPROD && warp == CW) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -295,6 +318,8 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
       }
+    } else if constexpr (kGPT == 0) {
+      if (tid < ng) bin_group<MODE, LUT>(buf + tid * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
     } else {
 #pragma unroll
       for (int j = 0; j < kGPT; ++j) {
@@ -303,7 +328,22 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    if constexpr (NOPROD) {
+      if (lane == 0 && atomicAdd(&sm.cnt[slot], 1u) == (uint32_t)(CW - 1)) {
+        // last warp out of this slot: refill it with stage i + STAGES
+        sm.cnt[slot] = 0u;
+        if (i + STAGES < n) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
+          const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * kStageGroups) * 48;
+          mbar_arrive_expect_tx(&sm.full[slot], bytes);
+          bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
+        }
+      }
+      if (i + STAGES < n) ahead.next(i + STAGES + 1 < n);
+    } else {
+      if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    }
     if (++slot == STAGES) {
       slot = 0;
       par ^= 1u;
@@ -340,8 +380,9 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 template <int MODE, int C>
 struct Cfg {
   static constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm, W = kCfgs[C].warps,
-                       L = kCfgs[C].lut, Q = kCfgs[C].quad;
-  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q>; }
+                       L = kCfgs[C].lut, Q = kCfgs[C].quad, NP = kCfgs[C].noprod;
+  static constexpr int kThreads = W * 32 + (NP ? 0 : 32);
+  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q, NP>; }
   static constexpr size_t smem() { return sizeof(K1Smem<S, L>); }
 };
 
@@ -349,7 +390,7 @@ template <int MODE, int C>
 cudaError_t launch_cfg(const HistSeg* d_segs, int32_t nseg, int64_t total_stages, uint32_t nh,
                        uint32_t ns, uint32_t nv, uint32_t* sink, int grid, cudaStream_t stream) {
   using K = Cfg<MODE, C>;
-  K::kernel()<<<grid, K::W * 32 + 32, K::smem(), stream>>>(d_segs, nseg, total_stages, nh, ns,
+  K::kernel()<<<grid, K::kThreads, K::smem(), stream>>>(d_segs, nseg, total_stages, nh, ns,
                                                              nv, kMadK, sink);
   return cudaGetLastError();
 }
@@ -362,7 +403,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
-    K1_CASE(9) K1_CASE(10) K1_CASE(11)
+    K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -389,7 +430,9 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 8>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 9>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 10>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 11>();
+  if ((e = configure_cfg<MODE, 11>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 12>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 13>();
 }
 
 }  // namespace
