@@ -242,6 +242,20 @@ def run_ours(args):
         ms_max = ms
     ms_step = ms_max / args.steps
 
+    # ---- read ceiling of K1's TMA pipeline on the same frames (K6, no binning)
+    read_gbs = None
+    if not args.no_read_ceiling:
+        with torch.cuda.stream(stream):
+            ctx.debug_read_roofline(frames)
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record(stream)
+            for _ in range(3):
+                ctx.debug_read_roofline(frames)
+            r1.record(stream)
+        torch.cuda.synchronize()
+        read_gbs = frame_bytes / (r0.elapsed_time(r1) / 3 * 1e-3) / 1e9
+        ctx.stats(reset=True)
+
     # ---- parity of the timed results against the oracle golden (rank 0's video is C2 video 0)
     parity = None
     gpath = os.path.join(ROOT, "tests", "golden", "C2.json")
@@ -310,11 +324,13 @@ def run_ours(args):
     k1_alg = frame_bytes + v.n * HIST_BYTES
     achieved = k1_alg / (k1_ms * 1e-3) / 1e9
     traffic = None
+    instr_px = None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
             traffic = int(tr["dram_bytes_per_alg_byte"] * k1_alg)
+            instr_px = tr.get("thread_instr_per_px")
         except Exception:
             traffic = None
     fps = world * v.n / (ms_step * 1e-3)
@@ -341,9 +357,12 @@ def run_ours(args):
         "hbm_gbs": round(gbs, 1),
         "frac_of_measured_hbm": round(gbs / peak, 4),
         "frac_of_8tbs": round(gbs / 8000.0, 4),
+        "read_ceiling_gbs": None if read_gbs is None else round(read_gbs, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k1_hist_kernel",
-                     "alg_bytes_per_launch": k1_alg, "launch_ms": round(k1_ms, 4), "peak_src": peak_src},
+                     "alg_bytes_per_launch": k1_alg, "launch_ms": round(k1_ms, 4), "peak_src": peak_src,
+                     "frac_of_read_ceiling": None if read_gbs is None else round(achieved / read_gbs, 4),
+                     "frac_of_8tbs": round(achieved / 8000.0, 4), "instr_per_px_ncu": instr_px},
         "kernel_ms_per_step": {"k1": round(st["k1_ms"] / args.steps, 4),
                                "k2": round(st["k2_ms"] / args.steps, 4),
                                "k3": round(st["k3_ms"] / args.steps, 4)},
@@ -469,6 +488,8 @@ def run_config(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": f"{args.config.upper()} (BASELINE.json configs)", "videos": len(vids),
+                   "lpt_imbalance_max_over_mean": round(max(sum(vids[i].n * vids[i].frame_bytes for i in a) for a in assign)
+                                                        / (sum(v.n * v.frame_bytes for v in vids) / world), 4),
                    "frames": total_frames, "frame_bytes": total_bytes,
                    "parallelism": f"LPT whole-video sharding over {world} GPU(s), one NCCL all-gather",
                    "timing": "CUDA events around whole steps (frames resident)" if all_resident else
@@ -487,6 +508,93 @@ def run_config(args):
     return 0
 
 
+# ---------------------------------------------------------------- one video split by frames (f2)
+def run_shard_frames(args):
+    """--shard-frames: the C2 video split into contiguous frame ranges over the
+    ranks (strong scaling of ONE long video).  Exchanges:
+    last histograms, L1 arrays and embeddings, each one NCCL all-gather."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from synth import manifest, torch_dev
+    from paper_2503_12964_b200 import Ctx
+    from paper_2503_12964_b200 import dist as cdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29599")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    synth.build(device=True)
+    v = manifest.c2_video(0)
+    if args.frames:
+        v = manifest.subsample(v, args.frames)
+    a, b = cdist.frame_shards(v.n, world)[rank]
+    table = torch_dev.frame_table(v, dev)
+    frames = torch.empty((b - a, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+    torch_dev.gen_frames(v, table, frames, t0=a, n=b - a)
+    emb = torch.empty((b - a, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+    torch_dev.gen_emb(v, table, emb, t0=a, n=b - a)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Ctx(device=local, stream=stream, timing=True)
+    out = [None]
+
+    def step():
+        with torch.cuda.stream(stream):
+            out[0] = cdist.run_video_sharded(ctx, frames, emb, v.n, a)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.stats(reset=True)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    st = ctx.stats(reset=True)
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    allt = torch.empty(world, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(allt, t)
+    per_rank = allt.cpu().tolist()
+    ms = max(per_rank)
+    if rank == 0:
+        parity = None
+        gpath = os.path.join(ROOT, "tests", "golden", "C2.json")
+        if not args.frames and os.path.exists(gpath):
+            g = json.load(open(gpath))["videos"][0]
+            parity = out[0][0] == g["detected"] and out[0][1] == g["final"]
+        line = {
+            "metric": METRIC, "value": round(v.n / (ms * 1e-3), 3), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": "C2: ONE 10-min 720p video split by frame ranges over the GPUs (SURVEY f2)",
+                       "frames": v.n, "frames_per_gpu": b - a,
+                       "parallelism": f"frame-range sharding over {world} GPU(s); NCCL all-gathers of "
+                                      "last histograms, L1 arrays and embeddings"},
+            "hbm_gbs": round(v.n * v.frame_bytes / (ms * 1e-3) / 1e9, 1),
+            "per_rank_ms_per_step": [round(x, 4) for x in per_rank],
+            "k1_ms_per_step_rank0": round(st["k1_ms"] / args.steps, 4),
+            "gpu_launches": int(st["launches"]), "clocks": clk.summary(), "parity_vs_golden": parity,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -500,14 +608,19 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gather", action="store_true", help="diagnosis: skip the result all-gather")
+    ap.add_argument("--no-read-ceiling", action="store_true")
     ap.add_argument("--config", default="", help="C3|C4|C5: strong-scaling batch run")
     ap.add_argument("--max-videos", type=int, default=0)
     ap.add_argument("--resident-gb", type=float, default=150.0)
+    ap.add_argument("--shard-frames", action="store_true",
+                    help="split the C2 video by frame ranges over the GPUs (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.config:
         return run_config(args)
+    if args.shard_frames:
+        return run_shard_frames(args)
     return run_ours(args)
 
 

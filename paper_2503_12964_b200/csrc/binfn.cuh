@@ -184,8 +184,8 @@ CD_HD uint32_t code_to_bin(uint32_t idx) {
 //   qr = floor(3 na / d) (rising sectors), qf = floor(3 (d - na) / d) (falling),
 // na = mid - min, d = max - min (entry 0 for grey).  The XOR spreads lanes
 // with equal na over the 32 banks.  Lane code layout (index = lane >> 3):
-//   bit 3 A, bits 4-7 q (qr | qf << 2), bits 8-9 v, bit 10 s1, bit 11 s2,
-//   bit 12 B, bits 13-14 0, bit 15 C   -> 5120 code indices used.
+//   bit 3 A, bits 4-7 q (qr | qf << 2), bits 8-9 v, bit 10 s1 = [3d >= max],
+//   bit 11 s2 = [3d >= 2 max], bit 12 B, bits 13-14 0, bit 15 C  -> 5120 code indices.
 constexpr int kLutCodeShift = 3;
 constexpr int kLutCodes = 5120;
 
@@ -214,10 +214,12 @@ CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t tA = cd_mad(G, k.neg1, R15);  // bit 15: r >= g   (IMAD)
   const uint32_t tB = G + kB15 - B;            // bit 15: g >= b   (IADD3)
   const uint32_t tC = cd_mad(B, k.neg1, R15);  // bit 15: r >= b   (IMAD)
-  const uint32_t mx1 = cd_max_u16x2(mx, 0x00010001u);
-  const uint32_t z1 = cd_mad(mx1, k.neg1, 0x04000400u);
-  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx1 + 2^10
-  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx1 + 2^11
+  // s flags against max itself: black (max = 0) sets both, but a grey pixel is
+  // recognisable from its table entry (qr = qf = 0 only when d = 0) and
+  // code_to_bin_lut forces s = 0 for it.
+  const uint32_t z1 = cd_mad(mx, k.neg1, 0x04000400u);
+  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10
+  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx + 2^11
   const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8,9 of 3 max = v
   const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
   return (ab & 0x10081008u) | (m3 & 0x03000300u) | (s1 & 0x04000400u) | (s2 & 0x08000800u) |
@@ -239,6 +241,7 @@ CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
   const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
   const uint32_t oidx = (A << 2) | (B << 1) | C;
   if (z || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
+  if (qr == 0u && qf == 0u) return oidx == 7u ? v : 255u;  // grey (d = 0): h = 0, s = 0
   const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
   return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
 }

@@ -88,3 +88,66 @@ def gather_results(results, capacity: int, device=None, group=None) -> list | No
     for r in range(world):
         allr.extend(unpack_results(arr[r]))
     return sorted(allr, key=lambda d: d["id"])
+
+
+# ---------------------------------------------------------------- intra-video sharding (NEXT f2)
+def frame_shards(n: int, world: int) -> list:
+    """Contiguous frame ranges [f0, f1) of one video over `world` ranks."""
+    return [(n * r // world, n * (r + 1) // world) for r in range(world)]
+
+
+def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_all=None):
+    """One long video split by frame ranges across the ranks of `group`
+    (the context-parallel analogue on the frame axis).
+
+    Every step of the path still runs in libclipdetect kernels; the exchanges are
+    NCCL collectives over NVLink:
+      1. K1 + L1 on the local shard (clip_frame_scores);
+      2. all_gather of each shard's last histogram -> L1 of each shard's first
+         frame against its predecessor (clip_frame_scores on that one frame
+         with prev_hist);
+      3. all_gather of the L1 arrays -> every rank runs clip_cuts on the whole
+         video's L1 (identical detected cuts everywhere);
+      4. all_gather of the embeddings -> clip_merge on the whole video.
+    Results are identical to the single-GPU path (same kernels, same order).
+    `frames`: u8 cuda [m, H, W, 3] = frames f0..f0+m-1; `emb`: f32 cuda [m, D].
+    Returns (detected list, final list, cos tensor, band hits, rounds)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m, H, W, _ = frames.shape
+    dev = frames.device
+    hist, l1, _ = ctx.frame_scores(frames, want_score=False)
+    nb = hist.shape[1]
+    # (2) last histograms of every shard
+    lasts = torch.empty(world * nb, dtype=hist.dtype, device=dev)
+    dist.all_gather_into_tensor(lasts, hist[m - 1].contiguous(), group=group)
+    lasts = lasts.view(world, nb)
+    if rank > 0:
+        _, l1_first, _ = ctx.frame_scores(frames[:1], prev_hist=lasts[rank - 1].contiguous(),
+                                          want_score=False)
+        l1[:1].copy_(l1_first)
+    # (3) whole-video L1 on every rank; shards are padded to a common length
+    shards = frame_shards(n_total, world)
+    width = max(b - a for a, b in shards)
+    pad = torch.zeros(width, dtype=l1.dtype, device=dev)
+    pad[:m].copy_(l1)
+    l1_all = torch.empty(world * width, dtype=l1.dtype, device=dev)
+    dist.all_gather_into_tensor(l1_all, pad, group=group)
+    l1_full = torch.cat([l1_all[r * width:r * width + (b - a)] for r, (a, b) in enumerate(shards)])
+    state = torch.zeros(4, dtype=torch.int64, device=dev)
+    cuts = torch.empty(n_total // ctx.params.min_clip_frames + 2, dtype=torch.int32, device=dev)
+    ctx.cuts(l1_full, H * W, state, cuts, True)
+    n_cuts = int(state[3].item())
+    # (4) embeddings of the whole video, then the merge
+    if emb_all is None:
+        D = emb.shape[1]
+        epad = torch.zeros((width, D), dtype=emb.dtype, device=dev)
+        epad[:m].copy_(emb)
+        e_all = torch.empty(world * width * D, dtype=emb.dtype, device=dev)
+        dist.all_gather_into_tensor(e_all, epad.view(-1), group=group)
+        e_all = e_all.view(world * width, D)
+        emb_all = torch.cat([e_all[r * width:r * width + (b - a)] for r, (a, b) in enumerate(shards)])
+    merged, cos, hits, rounds = ctx.merge(emb_all, cuts[:max(1, n_cuts)].contiguous(), n_cuts=n_cuts)
+    return (cuts[:n_cuts].cpu().tolist(), merged.cpu().tolist(), cos, hits, rounds)

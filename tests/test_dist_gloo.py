@@ -93,3 +93,83 @@ def test_gather_over_gloo(world):
     want = [(v, list(map(int, _fake(v, lengths[v]).detected)), list(map(int, _fake(v, lengths[v]).final)))
             for v in range(nvid)]
     assert got == want
+
+
+# ---------------------------------------------------------------- intra-video sharding (f2)
+class _OracleCtx:
+    """CPU stand-in for the Ctx binding (oracle-backed) so that the sharded
+    orchestration and its collectives can run under gloo without a GPU."""
+
+    class _P:
+        min_clip_frames = 8
+
+    params = _P()
+
+    def frame_scores(self, frames, prev_hist=None, want_score=True):
+        import oracle
+        import torch
+        f = frames.numpy()
+        h = oracle.hist_frames(f)
+        npix = f[0].size // 3
+        if prev_hist is not None:
+            hh = np.concatenate([prev_hist.numpy().view(np.uint32)[None], h])
+            l1, _ = oracle.l1(hh, npix)
+            l1 = l1[1:]
+        else:
+            l1, _ = oracle.l1(h, npix)
+        return (torch.from_numpy(h.view(np.int32).copy()), torch.from_numpy(l1.view(np.int32).copy()), None)
+
+    def cuts(self, l1, npix, state, cuts, is_final):
+        import oracle
+        a = l1.numpy().view(np.uint32)
+        det = oracle.min_length(oracle.candidates(a, npix), a.size, 8)
+        cuts[:det.size] = __import__("torch").from_numpy(det.astype(np.int32))
+        state[3] = det.size
+
+    def merge(self, emb, cuts, n_cuts):
+        import oracle
+        import torch
+        r = oracle.merge(emb.numpy(), cuts.numpy()[:n_cuts].astype(np.int64))
+        return torch.from_numpy(r.final.astype(np.int32)), torch.from_numpy(r.cos), r.n_band_hits, r.rounds
+
+
+def _shard_worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    v = manifest.subsample(manifest.c2_video(0), n)
+    v = manifest.Video(id=0, W=64, H=48, n=n, seed=v.seed, frames=v.frames, hard=v.hard, false=v.false)
+    a, b = cdist.frame_shards(n, world)[rank]
+    frames = torch.from_numpy(synth.gen_frames(v, t0=a, n=b - a))
+    emb = torch.from_numpy(synth.gen_emb(v, t0=a, n=b - a))
+    det, fin, cos, hits, rounds = cdist.run_video_sharded(_OracleCtx(), frames, emb, n, a)
+    if rank == 0:
+        q.put((det, fin, rounds))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_video_equals_whole_video(world):
+    import oracle
+    import synth
+    n = 700
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    det, fin, rounds = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    v = manifest.subsample(manifest.c2_video(0), n)
+    v = manifest.Video(id=0, W=64, H=48, n=n, seed=v.seed, frames=v.frames)
+    ref = oracle.run_video(synth.gen_frames(v), synth.gen_emb(v))
+    assert det == list(ref.detected) and fin == list(ref.final) and rounds == ref.rounds
+    assert len(det) > 3  # the split crosses real cuts

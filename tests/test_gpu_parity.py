@@ -342,3 +342,39 @@ def test_invalid_arguments_fail_without_side_effects(ctx, dev):
     frames, _ = _dev_video(v, dev, emb=False)
     ctx.frame_scores(frames)
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ K1 launch configurations
+@pytest.mark.parametrize("cfg", list(range(14)))
+def test_every_k1_config_matches_oracle(dev, cfg, monkeypatch):
+    """All K1 launch configurations (ring depth, CTAs/SM, warps, hue table,
+    lane layout, producer scheme) give the oracle's histograms, incl. ragged
+    stages (854x480) and the LUT/grey corner cases (flat frames)."""
+    from paper_2503_12964_b200 import Ctx
+    monkeypatch.setenv("CLIPDETECT_K1_CFG", str(cfg))
+    c = Ctx(device=0)
+    rng = np.random.default_rng(cfg)
+    host = rng.integers(0, 256, size=(6, 480, 854, 3), dtype=np.uint8)
+    host[1] = 0            # black
+    host[2] = 128          # grey
+    host[3, :, :, :] = (200, 200, 10)  # yellow edge (q = 3 in the rising sector)
+    v = manifest.c1_video()
+    c1 = synth.gen_frames(v)
+    for frames in (host, c1):
+        hist, l1, _ = c.frame_scores(torch.from_numpy(frames).to(dev))
+        assert np.array_equal(_u32(hist), oracle.hist_frames(frames)), cfg
+    got = c.debug_binmap().cpu().numpy()
+    want = oracle.bin_table()
+    assert np.array_equal(got[0], want) and np.array_equal(got[1], want)
+    c.close()
+
+
+def test_run_to_run_determinism(ctx, dev):
+    """Histograms, cuts and cosines are bit-identical across runs."""
+    v = manifest.subsample(manifest.c3_videos()[1], 300)
+    frames, emb = _dev_video(v, dev)
+    item = [{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb}]
+    a = ctx.run_videos(item, want_cos=True)[0]
+    b = ctx.run_videos(item, want_cos=True)[0]
+    assert list(a.detected) == list(b.detected) and list(a.final) == list(b.final)
+    assert np.array_equal(a.detected_cos, b.detected_cos)  # bitwise, not approx
