@@ -378,3 +378,26 @@ def test_run_to_run_determinism(ctx, dev):
     b = ctx.run_videos(item, want_cos=True)[0]
     assert list(a.detected) == list(b.detected) and list(a.final) == list(b.final)
     assert np.array_equal(a.detected_cos, b.detected_cos)  # bitwise, not approx
+
+
+def test_tiny_and_cutless_videos(ctx, dev):
+    """n = 1, n < 2 L_min, a flat video (no candidates) and a normal one in one
+    batch: empty cut lists where the oracle has none, merge with K = 1 clip."""
+    rng = np.random.default_rng(77)
+    items, refs = [], []
+    for n in [1, 3, 15, 40]:
+        if n == 40:
+            v = manifest.subsample(manifest.c1_video(), 40)
+            host = synth.gen_frames(v)
+        else:
+            host = np.broadcast_to(rng.integers(0, 256, size=(1, 1, 1, 3), dtype=np.uint8),
+                                   (n, 16, 32, 3)).copy()
+        emb = rng.standard_normal((n, 8)).astype(np.float32)
+        items.append({"n": n, "H": host.shape[1], "W": host.shape[2],
+                      "frames": torch.from_numpy(host).to(dev), "emb": torch.from_numpy(emb).to(dev)})
+        refs.append(oracle.run_video(host, emb))
+    res = ctx.run_videos(items, want_cos=True)
+    for r, ref in zip(res, refs):
+        assert list(r.detected) == list(ref.detected)
+        assert list(r.final) == list(ref.final)
+        assert r.rounds == ref.rounds

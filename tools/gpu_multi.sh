@@ -14,6 +14,7 @@ run() {  # name, port, args...
   fi
 }
 run bench_n$N 29511 --steps 30 --warmup 3 ${BENCH_EXTRA}
+run bench_shard_n$N 29514 --shard-frames --steps 30 --warmup 3
 for c in ${CONFIGS:-C3 C4 C5}; do
   run bench_${c}_n$N 29512 --config $c --steps 2 --warmup 1
 done
