@@ -44,8 +44,9 @@ struct K1Cfg {
 constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
                            {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
                            {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
-                           {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1}};
-constexpr int kNumCfgs = 14;
+                           {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1},
+                           {4, 1, 16, 1, 3}};
+constexpr int kNumCfgs = 15;
 
 template <int STAGES, int LUT>
 struct K1Smem {
@@ -200,6 +201,42 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   }
 }
 
+// NQ quads of one lane, phase by phase across all of them (loads, unpack,
+// codes, table lookups, atomics): NQ*2 independent pixel-pair chains in flight.
+template <int NQ>
+__device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qstride,
+                                              uint32_t* hist, const uint8_t* lut, MadK mk) {
+  uint32_t w[NQ][3];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(buf + (q0 + j * qstride) * 12);
+    w[j][0] = p[0];
+    w[j][1] = p[1];
+    w[j][2] = p[2];
+  }
+  uint32_t pre[2 * NQ], ia[2 * NQ], ib[2 * NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    uint32_t R01, G01, B01, R23, G23, B23;
+    unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
+    pre[2 * j] = code_pair_lut_pre(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_lut_pre(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+  }
+  uint32_t qa[2 * NQ], qb[2 * NQ];
+#pragma unroll
+  for (int j = 0; j < 2 * NQ; ++j) {
+    qa[j] = lut[ia[j]];
+    qb[j] = lut[ib[j]];
+  }
+  char* hb = reinterpret_cast<char*>(hist);
+#pragma unroll
+  for (int j = 0; j < 2 * NQ; ++j) {
+    const uint32_t c = code_pair_lut_post(pre[j], qa[j], qb[j], mk);
+    hist_inc(hb, lut_off_lo(c, mk));
+    hist_inc(hb, lut_off_hi(c, mk));
+  }
+}
+
 template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD>
 __global__ void __launch_bounds__(CW * 32 + (NOPROD ? 0 : 32), MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
@@ -308,6 +345,14 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const int nq = ng * 4;
 #pragma unroll 2
       for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+    } else if constexpr (QUAD == 3 && MODE == kModeFast && LUT) {
+      constexpr int kQPL = 4 * kStageGroups / kConsumers;
+      const int nq = ng * 4;
+      if (nq == kQPL * kConsumers) {
+        bin_quads_lut<kQPL>(buf, tid, kConsumers, wh, sm.lut, mk);
+      } else {
+        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+      }
     } else if constexpr (QUAD == 2 && MODE == kModeFast) {
       // all of a lane's quads of a full stage issued together (more independent work per warp)
       constexpr int kQPL = 4 * kStageGroups / kConsumers;
@@ -403,7 +448,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
-    K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13)
+    K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -432,7 +477,8 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 10>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 11>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 12>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 13>();
+  if ((e = configure_cfg<MODE, 13>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 14>();
 }
 
 }  // namespace
