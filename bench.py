@@ -602,7 +602,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=0, help="debug: truncate the C2 video")
-    ap.add_argument("--ref-frames", type=int, default=600, help="oracle sample frames per step")
+    ap.add_argument("--ref-frames", type=int, default=2400, help="oracle sample frames per step")
     ap.add_argument("--e2e-frames", type=int, default=18000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -194,11 +194,14 @@ CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
   const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
   return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
 }
-CD_HD uint32_t lut_index(uint32_t na, uint32_t d) { return d * 256u + (na ^ d); }
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d, bool swz = true) {
+  return d * 256u + (swz ? (na ^ d) : na);
+}
 
 // Part 1 (before the table lookups): returns the partial code and the two
 // lanes' table indices.  The sector is carried as the three raw ordering
 // flags A, B, C (parity is decoded from them in code_to_bin_lut).
+template <bool SWZ = true>
 CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   constexpr uint32_t kB15 = 0x80008000u;
@@ -207,7 +210,7 @@ CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t d = cd_mad(mn, k.neg1, mx);
   const uint32_t sum = cd_mad(B, k.one, cd_mad(R, k.one, G));
   const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, sum));  // mid - min
-  const uint32_t nas = na ^ d;                                        // bank swizzle
+  const uint32_t nas = SWZ ? (na ^ d) : na;                          // bank swizzle
   i0 = cd_prmt(nas, d, 0x1140u);  // lane 0: nas | d << 8
   i1 = cd_prmt(nas, d, 0x3362u);  // lane 1
   const uint32_t R15 = cd_mad(R, k.one, kB15);
