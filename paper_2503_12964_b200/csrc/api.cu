@@ -37,7 +37,7 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
-  int k1_cfg = 9;  // K1 launch configuration: LUT hue, lane-contiguous quads x4, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
+  int k1_cfg = 14;  // K1 launch configuration: LUT hue, staged lane-contiguous quads, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
   clip_stats stats{};
