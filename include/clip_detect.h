@@ -21,7 +21,13 @@
  *    effects).  CLIP_E_CUDA is sticky: the ctx must be destroyed.
  *    clip_last_error() gives a one-line message for the last failure.
  *  - Frames are decoded RGB24, u8 [n][H][W][3] contiguous, base 16-byte
- *    aligned, H*W % 16 == 0 (every resolution of the workloads satisfies it).
+ *    aligned, H*W % 16 == 0 (every resolution of the workloads satisfies it),
+ *    or (the *_nv12 entry points, clip_video.format = CLIP_FORMAT_NV12) the
+ *    decoder's NV12 surfaces, u8 [n][H*3/2][W] contiguous: H rows of Y, then
+ *    H/2 rows of interleaved U,V at half horizontal resolution; H and W even,
+ *    base 16-byte aligned, H*W % 32 == 0.  NV12 is converted to RGB by reading
+ *    O0 (BT.601 limited range, 20-bit fixed point = OpenCV COLOR_YUV2RGB_NV12)
+ *    inside the histogram kernel; the RGB frame is never materialised.
  *  - Only compute capability 10.0 (B200, sm_100a) is supported: any other
  *    device gives CLIP_E_ARCH.  There is no CPU fallback.
  *  - Results are deterministic: histograms, L1, cuts bit-identical for any
@@ -95,6 +101,14 @@ int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, in
                       int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
                       float* score);
 
+/* Rows a1-a4 as clip_frame_scores, for NV12 frames (device u8 [n_frames][height*3/2][width]).
+ * O0 conversion fused into the histogram kernel (fast path for the default
+ * 18x3x3 bins and width % 16 == 0; any other case runs a generic kernel with
+ * the same results).  Errors: CLIP_E_INVALID for odd height/width.  Async. */
+int clip_frame_scores_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                           int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
+                           float* score);
+
 /* Streaming cut state of one video; lives in DEVICE memory, zeroed by the
  * caller at video start and passed unchanged between chunks. */
 typedef struct {
@@ -134,7 +148,10 @@ int clip_merge(clip_ctx* ctx, const float* emb, int64_t n_frames, int32_t dim,
 
 /* ---------------------------------------------------------------- batch API */
 
-/* Frame source callback: fill dst (device, [n][H][W][3]) with frames
+#define CLIP_FORMAT_RGB24 0 /* u8 [n][H][W][3]                */
+#define CLIP_FORMAT_NV12 1  /* u8 [n][H*3/2][W] (see above)    */
+
+/* Frame source callback: fill dst (device, in the video's format) with frames
  * first_frame..first_frame+n-1 of video `video_index` on `stream`; return 0
  * on success.  Used when clip_video.frames is NULL. */
 typedef int (*clip_fill_fn)(void* user, int64_t video_index, int64_t first_frame, int64_t n,
@@ -143,9 +160,9 @@ typedef int (*clip_fill_fn)(void* user, int64_t video_index, int64_t first_frame
 typedef struct {
   int64_t id;             /* caller's id, copied to the result           */
   int64_t n_frames;       /* >= 1                                        */
-  int32_t height, width;  /* H*W % 16 == 0                               */
+  int32_t height, width;  /* H*W % 16 == 0 (NV12: H, W even, H*W % 32 == 0) */
   int32_t dim;            /* embedding dim (same for all videos) or 0    */
-  int32_t reserved;
+  int32_t format;         /* CLIP_FORMAT_RGB24 (0) or CLIP_FORMAT_NV12   */
   const uint8_t* frames;  /* device or host (pinned or pageable) pointer, or NULL = fill callback */
   const float* emb;       /* device [n_frames][dim] or NULL (no merge: final = detected) */
 } clip_video;
@@ -204,10 +221,20 @@ int clip_get_stats(clip_ctx* ctx, clip_stats* out, int reset);
  * = in lane 1 (identical for the generic bins).  Async. */
 int clip_debug_binmap(clip_ctx* ctx, uint8_t* table);
 
+/* Test hook (K5, NV12): the fused conversion + bin function over every
+ * (Y, U, V) into table (device u8 [2][1<<24], index (Y<<16)|(U<<8)|V):
+ * table[0] = Y evaluated in lane 0 of a pixel pair sharing chroma (U, V),
+ * table[1] = in lane 1 (the lane-0 pixel then has luma Y ^ 0x5A).  Async. */
+int clip_debug_nv12map(clip_ctx* ctx, uint8_t* table);
+
 /* Bench hook (K6): stream n_frames frames through K1's TMA pipeline without
  * binning (the read roofline of the same kernel skeleton).  Async. */
 int clip_debug_read_roofline(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames,
                              int32_t height, int32_t width);
+/* K6 for NV12 frames (the fused NV12 kernel's TMA pipeline without binning;
+ * needs width % 16 == 0).  Async. */
+int clip_debug_read_roofline_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames,
+                                  int32_t height, int32_t width);
 
 #ifdef __cplusplus
 }

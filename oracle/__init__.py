@@ -88,6 +88,8 @@ def lib():
             "oracle_merge": (I64, [P, I64, I64, P, I64, F64, F64, I32, P, P, P, P]),
             "oracle_video": (ctypes.c_int, [P, I64, I64, P, I64, P, ctypes.c_int, P, P, P, P,
                                             P, P, P]),
+            "oracle_nv12_to_rgb": (None, [P, I64, I64, P]),
+            "oracle_hist_nv12_frames": (None, [P, I64, I64, I64, I32, I32, I32, P, ctypes.c_int]),
         }
         for name, (res, args) in sigs.items():
             f = getattr(L, name)
@@ -135,6 +137,41 @@ def hist_frames(frames: np.ndarray, p: Params = Params(), nthreads: int | None =
     out = np.empty((n, p.nbins), dtype=np.uint32)
     lib().oracle_hist_frames(_p(f), n, npix, p.nh, p.ns, p.nv, _p(out), _nthreads(nthreads))
     return out
+
+
+# ---------------------------------------------------------------- O0 (NV12)
+def nv12_to_rgb(frame: np.ndarray) -> np.ndarray:
+    """One NV12 frame u8 [H*3/2, W] -> RGB24 u8 [H, W, 3] (reading O0)."""
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    H, W = f.shape[0] * 2 // 3, f.shape[1]
+    out = np.empty((H, W, 3), dtype=np.uint8)
+    lib().oracle_nv12_to_rgb(_p(f), H, W, _p(out))
+    return out
+
+
+def hist_nv12_frames(frames: np.ndarray, p: Params = Params(), nthreads: int | None = None) -> np.ndarray:
+    """O0 + O2 for n NV12 frames u8 [n, H*3/2, W] -> [n, nbins]."""
+    f = np.ascontiguousarray(frames, dtype=np.uint8)
+    n = f.shape[0]
+    H, W = f.shape[1] * 2 // 3, f.shape[2]
+    out = np.empty((n, p.nbins), dtype=np.uint32)
+    lib().oracle_hist_nv12_frames(_p(f), n, H, W, p.nh, p.ns, p.nv, _p(out), _nthreads(nthreads))
+    return out
+
+
+def run_video_nv12(frames: np.ndarray, emb: np.ndarray | None, p: Params = Params(),
+                   nthreads: int | None = None) -> VideoResult:
+    """The whole path (O0 then O1..O9) for one NV12 video u8 [n, H*3/2, W]."""
+    h = hist_nv12_frames(frames, p, nthreads)
+    n = h.shape[0]
+    npix = frames.shape[2] * frames.shape[1] * 2 // 3
+    l1_, sc = l1(h, npix)
+    cand = candidates(l1_, npix, p)
+    det = min_length(cand, n, p.l_min)
+    if emb is None:
+        return VideoResult(h, l1_, sc, int(cand.size), det, det.copy(), np.zeros(det.size), 0, 0)
+    m = merge(emb, det, p)
+    return VideoResult(h, l1_, sc, int(cand.size), det, m.final, m.cos, m.n_band_hits, m.rounds)
 
 
 # ---------------------------------------------------------------- O3..O6

@@ -70,6 +70,42 @@ void oracle_bin_table(int32_t nh, int32_t ns, int32_t nv, uint8_t* table) {
         table[(r << 16) | (g << 8) | b] = (uint8_t)oracle_bin(r, g, b, nh, ns, nv);
 }
 
+/* ------------------------------------------------------------------ O0 --
+ * NV12 -> RGB (reading O0, for NVDEC-native input, §2.3):
+ * BT.601 limited range, 20-bit fixed point:
+ *   y' = max(0, Y - 16) * 1220542
+ *   R = sat((y' + 2^19 + 1673527 (V-128)) >> 20)
+ *   G = sat((y' + 2^19 - 852492 (V-128) - 409993 (U-128)) >> 20)
+ *   B = sat((y' + 2^19 + 2116026 (U-128)) >> 20)
+ * with sat() clamping to [0, 255] and >> an arithmetic (floor) shift; the
+ * chroma of pixel (x, y) is the UV pair of block (x/2, y/2). */
+static int32_t sat255(int64_t v) { return v < 0 ? 0 : (v > 255 ? 255 : (int32_t)v); }
+
+static int64_t floor_shift20(int64_t v) {
+  /* floor(v / 2^20) for any sign */
+  return v >= 0 ? v / 1048576 : -((-v + 1048575) / 1048576);
+}
+
+void oracle_nv12_to_rgb(const uint8_t* nv12, int64_t H, int64_t W, uint8_t* rgb) {
+  const uint8_t* Yp = nv12;
+  const uint8_t* UVp = nv12 + H * W;
+  for (int64_t y = 0; y < H; ++y) {
+    for (int64_t x = 0; x < W; ++x) {
+      int64_t Y = Yp[y * W + x];
+      int64_t U = UVp[(y / 2) * W + 2 * (x / 2)];
+      int64_t V = UVp[(y / 2) * W + 2 * (x / 2) + 1];
+      int64_t yy = (Y - 16 > 0 ? Y - 16 : 0) * 1220542;
+      int64_t r = yy + 524288 + 1673527 * (V - 128);
+      int64_t g = yy + 524288 - 852492 * (V - 128) - 409993 * (U - 128);
+      int64_t b = yy + 524288 + 2116026 * (U - 128);
+      uint8_t* o = rgb + 3 * (y * W + x);
+      o[0] = (uint8_t)sat255(floor_shift20(r));
+      o[1] = (uint8_t)sat255(floor_shift20(g));
+      o[2] = (uint8_t)sat255(floor_shift20(b));
+    }
+  }
+}
+
 /* ------------------------------------------------------------------ O2 --
  * hist_t[b] = #{pixels of frame t with bin b}; every pixel is analysed
  * (no downscaling, cropping or letterbox handling). */
@@ -123,6 +159,51 @@ void oracle_hist_frames(const uint8_t* frames, int64_t n, int64_t npix, int32_t 
     return;
   }
   for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, hist_worker, &jobs[i]);
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
+typedef struct {
+  const uint8_t* frames;
+  int64_t f0, f1, H, W;
+  int32_t nh, ns, nv;
+  uint32_t* hist;
+} nv12_job;
+
+static void* nv12_hist_worker(void* arg) {
+  nv12_job* j = (nv12_job*)arg;
+  int32_t nbins = j->nh * j->ns * j->nv;
+  uint8_t* rgb = (uint8_t*)malloc((size_t)(3 * j->H * j->W));
+  for (int64_t f = j->f0; f < j->f1; ++f) {
+    oracle_nv12_to_rgb(j->frames + f * (j->H * j->W * 3 / 2), j->H, j->W, rgb);
+    oracle_hist(rgb, j->H * j->W, j->nh, j->ns, j->nv, j->hist + f * nbins);
+  }
+  free(rgb);
+  return NULL;
+}
+
+void oracle_hist_nv12_frames(const uint8_t* frames, int64_t n, int64_t H, int64_t W, int32_t nh,
+                             int32_t ns, int32_t nv, uint32_t* hist, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (nthreads > n) nthreads = (int)(n > 0 ? n : 1);
+  pthread_t th[256];
+  nv12_job jobs[256];
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i].frames = frames;
+    jobs[i].f0 = n * i / nthreads;
+    jobs[i].f1 = n * (i + 1) / nthreads;
+    jobs[i].H = H;
+    jobs[i].W = W;
+    jobs[i].nh = nh;
+    jobs[i].ns = ns;
+    jobs[i].nv = nv;
+    jobs[i].hist = hist;
+  }
+  if (nthreads == 1) {
+    nv12_hist_worker(&jobs[0]);
+    return;
+  }
+  for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, nv12_hist_worker, &jobs[i]);
   for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
 }
 

@@ -30,6 +30,15 @@ typedef struct {
   int32_t max_rounds;          /* 0 = merge until fixed point */
 } oracle_params;
 
+/* O0 (NV12 input, NEXT f1): one NV12 frame (Y plane [H][W], then the
+ * interleaved UV plane [H/2][W/2][2]) -> RGB24 [H][W][3], BT.601 limited range
+ * in 20-bit fixed point (the definition of OpenCV's COLOR_YUV2RGB_NV12). */
+void oracle_nv12_to_rgb(const uint8_t* nv12, int64_t H, int64_t W, uint8_t* rgb);
+
+/* O0 + O2: histograms of n NV12 frames ([n][H*W*3/2] bytes) -> [n][nbins]. */
+void oracle_hist_nv12_frames(const uint8_t* frames, int64_t n, int64_t H, int64_t W, int32_t nh,
+                             int32_t ns, int32_t nv, uint32_t* hist, int nthreads);
+
 /* O1: pixel -> joint HSV bin in [0, nh*ns*nv). */
 int32_t oracle_bin(int32_t r, int32_t g, int32_t b, int32_t nh, int32_t ns, int32_t nv);
 

@@ -39,7 +39,7 @@ class ClipParams(ctypes.Structure):
 
 class ClipVideo(ctypes.Structure):
     _fields_ = [("id", ctypes.c_int64), ("n_frames", ctypes.c_int64), ("height", ctypes.c_int32),
-                ("width", ctypes.c_int32), ("dim", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("dim", ctypes.c_int32), ("format", ctypes.c_int32),
                 ("frames", ctypes.c_void_p), ("emb", ctypes.c_void_p)]
 
 
@@ -69,7 +69,11 @@ FILL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes
 
 EXPORTS = ["clip_params_default", "clip_detect_init", "clip_detect_destroy", "clip_last_error",
            "clip_frame_scores", "clip_cuts", "clip_merge", "clip_run_videos", "clip_get_stats",
-           "clip_debug_binmap", "clip_debug_read_roofline"]
+           "clip_debug_binmap", "clip_debug_read_roofline", "clip_frame_scores_nv12",
+           "clip_debug_nv12map", "clip_debug_read_roofline_nv12"]
+
+FORMAT_RGB24 = 0
+FORMAT_NV12 = 1
 
 _lib = None
 
@@ -103,6 +107,9 @@ def load(build_if_missing: bool = False):
     L.clip_get_stats.argtypes = [vp, ctypes.POINTER(ClipStats), ctypes.c_int]
     L.clip_debug_binmap.argtypes = [vp, vp]
     L.clip_debug_read_roofline.argtypes = [vp, vp, i64, i32, i32]
+    L.clip_frame_scores_nv12.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp]
+    L.clip_debug_nv12map.argtypes = [vp, vp]
+    L.clip_debug_read_roofline_nv12.argtypes = [vp, vp, i64, i32, i32]
     for name in EXPORTS:
         if name not in ("clip_params_default", "clip_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -199,6 +206,24 @@ class Ctx:
                                                 _ptr(hist), _ptr(l1), _ptr(score)))
         return hist, l1, score
 
+    def frame_scores_nv12(self, frames, prev_hist=None, hist=None, l1=None, score=None,
+                          want_l1: bool = True, want_score: bool = True):
+        """clip_frame_scores_nv12: rows a1-a4 for NV12 frames u8 [n, H*3/2, W] (reading O0)."""
+        import torch
+        n, H3, W = frames.shape
+        assert H3 % 3 == 0 and frames.dtype == torch.uint8 and frames.is_cuda
+        H = H3 * 2 // 3
+        dev = frames.device
+        if hist is None:
+            hist = torch.empty((n, self.nbins), dtype=torch.int32, device=dev)
+        if l1 is None and want_l1:
+            l1 = torch.empty(n, dtype=torch.int32, device=dev)
+        if score is None and want_score:
+            score = torch.empty(n, dtype=torch.float32, device=dev)
+        self._check(self._lib.clip_frame_scores_nv12(self._h, _ptr(frames), n, H, W, _ptr(prev_hist),
+                                                     _ptr(hist), _ptr(l1), _ptr(score)))
+        return hist, l1, score
+
     def cuts(self, l1, pixels_per_frame: int, state, cuts, is_final: bool):
         """clip_cuts: rows a5-a6 streaming; state is a device int64[4] tensor."""
         n = 0 if l1 is None else l1.numel()
@@ -226,7 +251,7 @@ class Ctx:
                    want_cos: bool = False, min_clip_frames: int | None = None) -> list:
         """clip_run_videos: rows a1-a9 for a batch.  ``videos``: dicts with
         keys n, H, W, frames (device tensor / numpy array / None), emb (device
-        tensor or None), id."""
+        tensor or None), id, format (FORMAT_RGB24 default / FORMAT_NV12)."""
         nv = len(videos)
         arr = (ClipVideo * nv)()
         L = min_clip_frames or self.params.min_clip_frames
@@ -238,6 +263,7 @@ class Ctx:
             arr[i].height = v["H"]
             arr[i].width = v["W"]
             arr[i].dim = 0 if e is None else e.shape[1]
+            arr[i].format = v.get("format", FORMAT_RGB24)
             arr[i].frames = _ptr(v.get("frames"))
             arr[i].emb = _ptr(e)
             cap += 2 * (v["n"] // L + 1)
@@ -280,3 +306,14 @@ class Ctx:
     def debug_read_roofline(self, frames):
         n, H, W, _ = frames.shape
         self._check(self._lib.clip_debug_read_roofline(self._h, _ptr(frames), n, H, W))
+
+    def debug_nv12map(self):
+        """K5 for NV12: [2, 1<<24] bins of every (Y, U, V) in lane 0 / lane 1."""
+        import torch
+        t = torch.empty(2 << 24, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._check(self._lib.clip_debug_nv12map(self._h, _ptr(t)))
+        return t.view(2, 1 << 24)
+
+    def debug_read_roofline_nv12(self, frames):
+        n, H3, W = frames.shape
+        self._check(self._lib.clip_debug_read_roofline_nv12(self._h, _ptr(frames), n, H3 * 2 // 3, W))

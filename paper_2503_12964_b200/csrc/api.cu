@@ -42,7 +42,7 @@ struct clip_ctx {
   std::string err;
   clip_stats stats{};
   // scratch
-  DevBuf segs, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
+  DevBuf segs, segs2, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
       detcos, pack, pack_cos, sink;
   DevBuf m_video, m_clip_video, m_f0, m_f1, m_piece_base, m_P, m_S, m_alive, m_alive2, m_cos_b,
       m_cos_clip, m_counters, m_vstate, m_valive;
@@ -215,6 +215,43 @@ int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   return CLIP_OK;
 }
 
+// One K1 launch per kernel kind over a list of NV12 segments: the fused TMA
+// kernel for the segments it supports, the generic kernel for the rest.
+int launch_k1_nv12(clip_ctx* ctx, const std::vector<Nv12Seg>& all, int mode) {
+  const clip_params& p = ctx->p;
+  std::vector<Nv12Seg> lists[2];  // 0 = fused (fast / read), 1 = generic
+  for (const Nv12Seg& s0 : all) {
+    Nv12Seg s = s0;
+    const bool fast = mode == kModeRead || (mode == kModeFast && nv12_fast_ok(s.width, p.h_bins, p.s_bins, p.v_bins));
+    s.rows = fast ? nv12_stage_rows(s.width) : nv12_generic_rows();
+    s.stages = (s.height / 2 + s.rows - 1) / s.rows;
+    lists[fast ? 0 : 1].push_back(s);
+  }
+  for (int k = 0; k < 2; ++k) {
+    auto& segs = lists[k];
+    if (segs.empty()) continue;
+    int64_t total = 0;
+    for (auto& s : segs) {
+      s.stage_base = total;
+      total += s.n_frames * s.stages;
+    }
+    CKS(ensure(ctx, k ? ctx->segs2 : ctx->segs, segs.size() * sizeof(Nv12Seg)));
+    DevBuf& db = k ? ctx->segs2 : ctx->segs;
+    CK(cudaMemcpyAsync(db.p, segs.data(), segs.size() * sizeof(Nv12Seg), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CKS(ensure(ctx, ctx->sink, 16));
+    Span sp(ctx, 0);
+    CK(k1_nv12_launch(k ? kModeGeneric : mode, P<Nv12Seg>(db), (int32_t)segs.size(), total,
+                      p.h_bins, p.s_bins, p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count,
+                      ctx->stream));
+    sp.end();
+    ctx->stats.k1_launches += 1;
+    ctx->stats.launches += 1;
+    for (auto& s : segs) ctx->stats.k1_bytes += s.n_frames * (int64_t)s.height * s.width * 3 / 2;
+  }
+  return CLIP_OK;
+}
+
 int validate_params(clip_ctx* ctx, const clip_params* p) {
   if (!p) return fail(ctx, CLIP_E_INVALID, "params is NULL");
   if (p->abi_version != CLIP_ABI_VERSION)
@@ -233,11 +270,16 @@ int validate_params(clip_ctx* ctx, const clip_params* p) {
 }
 
 int validate_frames(clip_ctx* ctx, const void* frames, int64_t n, int32_t h, int32_t w,
-                    bool allow_null) {
+                    bool allow_null, int format = CLIP_FORMAT_RGB24) {
   if (n < 1) return fail(ctx, CLIP_E_INVALID, "n_frames must be >= 1 (got %lld)", (long long)n);
   if (h < 1 || w < 1) return fail(ctx, CLIP_E_INVALID, "bad frame size %dx%d", w, h);
-  if (((int64_t)h * w) % 16 != 0)
-    return fail(ctx, CLIP_E_INVALID, "H*W = %lld is not a multiple of 16", (long long)h * w);
+  if (format != CLIP_FORMAT_RGB24 && format != CLIP_FORMAT_NV12)
+    return fail(ctx, CLIP_E_INVALID, "unknown frame format %d", format);
+  if (format == CLIP_FORMAT_NV12 && ((h | w) & 1))
+    return fail(ctx, CLIP_E_INVALID, "NV12 needs even height and width (got %dx%d)", w, h);
+  if (((int64_t)h * w) % (format == CLIP_FORMAT_NV12 ? 32 : 16) != 0)
+    return fail(ctx, CLIP_E_INVALID, "H*W = %lld is not a multiple of %d", (long long)h * w,
+                format == CLIP_FORMAT_NV12 ? 32 : 16);
   if ((int64_t)h * w > (1ll << 31)) return fail(ctx, CLIP_E_INVALID, "frame too large");
   if (!frames && !allow_null) return fail(ctx, CLIP_E_INVALID, "frames is NULL");
   if (frames && ((uintptr_t)frames & 15)) return fail(ctx, CLIP_E_INVALID, "frames not 16-byte aligned");
@@ -400,6 +442,7 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
     if (c >= 0 && c < k1_num_cfgs()) ctx->k1_cfg = c;
   }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
+      k1_nv12_configure() != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return CLIP_E_CUDA;
@@ -416,7 +459,7 @@ int clip_detect_destroy(clip_ctx* ctx) {
   if (!ctx) return CLIP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  DevBuf* bufs[] = {&ctx->segs, &ctx->vids, &ctx->hist, &ctx->l1, &ctx->cand_slots,
+  DevBuf* bufs[] = {&ctx->segs, &ctx->segs2, &ctx->vids, &ctx->hist, &ctx->l1, &ctx->cand_slots,
                     &ctx->cand_count, &ctx->cuts, &ctx->ncuts, &ctx->ncand, &ctx->final_cuts,
                     &ctx->nfinal, &ctx->detcos, &ctx->pack, &ctx->pack_cos, &ctx->sink,
                     &ctx->m_video, &ctx->m_clip_video, &ctx->m_f0, &ctx->m_f1,
@@ -438,21 +481,30 @@ int clip_detect_destroy(clip_ctx* ctx) {
 
 const char* clip_last_error(const clip_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
-int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
-                      int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
-                      float* score) {
+}  // extern "C"
+
+namespace {
+int frame_scores(clip_ctx* ctx, int format, const uint8_t* frames, int64_t n_frames,
+                 int32_t height, int32_t width, const uint32_t* prev_hist, uint32_t* hist,
+                 uint32_t* l1, float* score) {
   CKS(check_ctx(ctx));
-  CKS(validate_frames(ctx, frames, n_frames, height, width, false));
+  CKS(validate_frames(ctx, frames, n_frames, height, width, false, format));
   if (!hist) return fail(ctx, CLIP_E_INVALID, "hist is NULL");
   const uint32_t nbins = nbins_of(ctx->p);
   const int64_t npix = (int64_t)height * width;
   CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins * n_frames, ctx->stream));
-  std::vector<HistSeg> segs(1);
-  segs[0].frames = frames;
-  segs[0].hist = hist;
-  segs[0].n_frames = n_frames;
-  segs[0].groups = npix / 16;
-  CKS(launch_k1(ctx, segs, k1_mode(ctx->p)));
+  if (format == CLIP_FORMAT_NV12) {
+    std::vector<Nv12Seg> segs(1);
+    segs[0] = Nv12Seg{frames, hist, n_frames, height, width, 0, 0, 0};
+    CKS(launch_k1_nv12(ctx, segs, k1_mode(ctx->p)));
+  } else {
+    std::vector<HistSeg> segs(1);
+    segs[0].frames = frames;
+    segs[0].hist = hist;
+    segs[0].n_frames = n_frames;
+    segs[0].groups = npix / 16;
+    CKS(launch_k1(ctx, segs, k1_mode(ctx->p)));
+  }
   if (l1 || score) {
     VideoDesc vd{0, n_frames, npix};
     CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
@@ -464,6 +516,23 @@ int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, in
     ctx->stats.launches += 1;
   }
   return CLIP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                      int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
+                      float* score) {
+  return frame_scores(ctx, CLIP_FORMAT_RGB24, frames, n_frames, height, width, prev_hist, hist,
+                      l1, score);
+}
+
+int clip_frame_scores_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                           int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
+                           float* score) {
+  return frame_scores(ctx, CLIP_FORMAT_NV12, frames, n_frames, height, width, prev_hist, hist,
+                      l1, score);
 }
 
 int clip_cuts(clip_ctx* ctx, const uint32_t* l1, int64_t n_frames, int64_t pixels_per_frame,
@@ -538,7 +607,7 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
   const int64_t L = ctx->p.min_clip_frames;
   for (int32_t i = 0; i < n_videos; ++i) {
     const clip_video& v = videos[i];
-    CKS(validate_frames(ctx, v.frames, v.n_frames, v.height, v.width, fill != nullptr));
+    CKS(validate_frames(ctx, v.frames, v.n_frames, v.height, v.width, fill != nullptr, v.format));
     if (v.dim != dim) return fail(ctx, CLIP_E_INVALID, "video %d: dim %d != %d", i, v.dim, dim);
     if (merge && !v.emb) return fail(ctx, CLIP_E_INVALID, "video %d: emb is NULL", i);
     if (dim < 0 || dim > 65536) return fail(ctx, CLIP_E_INVALID, "bad dim %d", dim);
@@ -587,10 +656,14 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
 
   // ---- K1: device-resident videos in one launch
   std::vector<HistSeg> segs;
+  std::vector<Nv12Seg> nsegs;
   std::vector<int32_t> streamed;
   for (int32_t i = 0; i < n_videos; ++i) {
     const clip_video& v = videos[i];
-    if (v.frames && is_device_ptr(v.frames)) {
+    if (v.frames && is_device_ptr(v.frames) && v.format == CLIP_FORMAT_NV12) {
+      nsegs.push_back(Nv12Seg{v.frames, d_hist + vd[i].fbase * nbins, v.n_frames, v.height,
+                              v.width, 0, 0, 0});
+    } else if (v.frames && is_device_ptr(v.frames)) {
       HistSeg s{};
       s.frames = v.frames;
       s.hist = d_hist + vd[i].fbase * nbins;
@@ -602,18 +675,22 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
     }
   }
   CKS(launch_k1(ctx, segs, mode));
+  CKS(launch_k1_nv12(ctx, nsegs, mode));
 
   // ---- K1: host / callback videos, chunk by chunk through two staging buffers
   if (!streamed.empty()) {
     int64_t max_fb = 0;
-    for (int32_t i : streamed) max_fb = std::max<int64_t>(max_fb, 3 * vd[i].npix);
+    auto frame_bytes = [&](int32_t i) {
+      return videos[i].format == CLIP_FORMAT_NV12 ? 3 * vd[i].npix / 2 : 3 * vd[i].npix;
+    };
+    for (int32_t i : streamed) max_fb = std::max<int64_t>(max_fb, frame_bytes(i));
     int64_t cf = chunk_frames > 0 ? chunk_frames : std::max<int64_t>(1, ((int64_t)1 << 30) / max_fb);
     CKS(ensure(ctx, ctx->staging[0], cf * max_fb));
     CKS(ensure(ctx, ctx->staging[1], cf * max_fb));
     int chunk_i = 0;
     for (int32_t i : streamed) {
       const clip_video& v = videos[i];
-      const int64_t fb = 3 * vd[i].npix;
+      const int64_t fb = frame_bytes(i);
       for (int64_t t0 = 0; t0 < v.n_frames; t0 += cf, ++chunk_i) {
         const int64_t m = std::min(cf, v.n_frames - t0);
         const int b = chunk_i & 1;
@@ -630,12 +707,18 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
             return fail(ctx, CLIP_E_INVALID, "fill callback failed (video %d, frame %lld)", i,
                         (long long)t0);
         }
-        std::vector<HistSeg> one(1);
-        one[0].frames = dst;
-        one[0].hist = d_hist + (vd[i].fbase + t0) * nbins;
-        one[0].n_frames = m;
-        one[0].groups = vd[i].npix / 16;
-        CKS(launch_k1(ctx, one, mode));
+        if (v.format == CLIP_FORMAT_NV12) {
+          std::vector<Nv12Seg> one(1);
+          one[0] = Nv12Seg{dst, d_hist + (vd[i].fbase + t0) * nbins, m, v.height, v.width, 0, 0, 0};
+          CKS(launch_k1_nv12(ctx, one, mode));
+        } else {
+          std::vector<HistSeg> one(1);
+          one[0].frames = dst;
+          one[0].hist = d_hist + (vd[i].fbase + t0) * nbins;
+          one[0].n_frames = m;
+          one[0].groups = vd[i].npix / 16;
+          CKS(launch_k1(ctx, one, mode));
+        }
         CK(cudaEventRecord(ctx->consumed[b], ctx->stream));
       }
     }
@@ -749,6 +832,26 @@ int clip_debug_binmap(clip_ctx* ctx, uint8_t* table) {
                       k1_mode(ctx->p) == kModeFast, k1_cfg_uses_lut(ctx->k1_cfg), ctx->stream));
   ctx->stats.launches += 1;
   return CLIP_OK;
+}
+
+int clip_debug_nv12map(clip_ctx* ctx, uint8_t* table) {
+  CKS(check_ctx(ctx));
+  if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
+  CK(k5_nv12map_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
+                       k1_mode(ctx->p) == kModeFast, ctx->stream));
+  ctx->stats.launches += 1;
+  return CLIP_OK;
+}
+
+int clip_debug_read_roofline_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames,
+                                  int32_t height, int32_t width) {
+  CKS(check_ctx(ctx));
+  CKS(validate_frames(ctx, frames, n_frames, height, width, false, CLIP_FORMAT_NV12));
+  if (width % 16 != 0 || nv12_stage_rows(width) < 1)
+    return fail(ctx, CLIP_E_INVALID, "NV12 read roofline needs width %% 16 == 0 and <= 8192");
+  std::vector<Nv12Seg> segs(1);
+  segs[0] = Nv12Seg{frames, nullptr, n_frames, height, width, 0, 0, 0};
+  return launch_k1_nv12(ctx, segs, kModeRead);
 }
 
 int clip_debug_read_roofline(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames,

@@ -249,6 +249,52 @@ CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
   return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
 }
 
+// ------------------------------------------------------------ NV12 input (NEXT f1)
+// Reading O0: NVDEC's NV12 (Y plane + interleaved UV at half resolution) ->
+// RGB by BT.601 limited range in 20-bit fixed point (OpenCV's
+// COLOR_YUV2RGB_NV12):  y' = max(0, Y-16)*1220542,  R = sat((y' + ruv) >> 20),
+// G = sat((y' + guv) >> 20), B = sat((y' + buv) >> 20) with the chroma terms
+// below (int32 throughout: |y' + c| < 2^30).  Two horizontally adjacent pixels
+// share one chroma sample, so the pair comes out directly as u16x2 lanes.
+constexpr int32_t kCY = 1220542;
+CD_HD void nv12_chroma(uint32_t U, uint32_t V, int32_t& ruv, int32_t& guv, int32_t& buv) {
+  ruv = 1673527 * (int32_t)V + (524288 - 128 * 1673527);
+  guv = -852492 * (int32_t)V - 409993 * (int32_t)U + (524288 + 128 * 852492 + 128 * 409993);
+  buv = 2116026 * (int32_t)U + (524288 - 128 * 2116026);
+}
+CD_HD int32_t nv12_luma(uint32_t Y) {
+#if defined(__CUDA_ARCH__)
+  return __viaddmax_s32((int32_t)Y, -16, 0) * kCY;  // VIADDMNMX
+#else
+  const int32_t y = (int32_t)Y - 16;
+  return (y > 0 ? y : 0) * kCY;
+#endif
+}
+// Per signed 16-bit lane: clamp to [0, 255].
+CD_HD uint32_t cd_sat_u8_s16x2(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  return __vimin_s16x2_relu(x, 0x00FF00FFu);  // VIMNMX.S16x2.RELU
+#else
+  uint32_t out = 0;
+  for (int l = 0; l < 2; ++l) {
+    int32_t v = (int16_t)(x >> (16 * l));
+    v = v < 0 ? 0 : (v > 255 ? 255 : v);
+    out |= (uint32_t)v << (16 * l);
+  }
+  return out;
+#endif
+}
+CD_HD uint32_t nv12_chan_pair(int32_t la, int32_t lb, int32_t c) {
+  return cd_sat_u8_s16x2(cd_prmt((uint32_t)((la + c) >> 20), (uint32_t)((lb + c) >> 20), 0x5410u));
+}
+CD_HD void nv12_pair_rgb(uint32_t ya, uint32_t yb, int32_t ruv, int32_t guv, int32_t buv,
+                         uint32_t& R, uint32_t& G, uint32_t& B) {
+  const int32_t la = nv12_luma(ya), lb = nv12_luma(yb);
+  R = nv12_chan_pair(la, lb, ruv);
+  G = nv12_chan_pair(la, lb, guv);
+  B = nv12_chan_pair(la, lb, buv);
+}
+
 // Pack 4 pixels (12 bytes in words w0, w1, w2) into two u16x2 pairs:
 // (R01, G01, B01) = pixels 0,1 and (R23, G23, B23) = pixels 2,3.
 CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,

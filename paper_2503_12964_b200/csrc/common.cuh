@@ -80,4 +80,17 @@ struct HistSeg {
   int64_t stage_base;    // prefix of n_frames*stages over earlier segments
 };
 
+// NV12 segment (NEXT f1): frames u8 [n][H*3/2][W] (Y rows, then H/2 rows of
+// interleaved UV), H and W even.  A stage = `rows` chroma-block rows of one
+// frame (2*rows Y rows + rows UV rows).
+struct Nv12Seg {
+  const uint8_t* frames;  // device
+  uint32_t* hist;         // device, [n][nbins]
+  int64_t n_frames;
+  int32_t height, width;
+  int32_t rows;           // block rows per stage (fast kernel; 0 for the generic one)
+  int32_t stages;         // stages per frame = ceil((H/2) / rows)
+  int64_t stage_base;     // prefix of n_frames*stages over earlier segments
+};
+
 }  // namespace clipdetect

@@ -22,6 +22,19 @@ int k1_cfg_uses_lut(int cfg);
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                              int lut, cudaStream_t stream);
 
+// ---- K1 for NV12 input (hist_nv12.cu)
+int nv12_stage_rows(int32_t width);
+bool nv12_fast_ok(int32_t width, uint32_t nh, uint32_t ns, uint32_t nv);
+int nv12_generic_rows();
+cudaError_t k1_nv12_configure();
+// mode kModeFast / kModeRead: persistent TMA kernel over `total` stages;
+// kModeGeneric: generic kernel over `total` (frame, 8-block-row) items.
+cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
+                           uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
+                           cudaStream_t stream);
+cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
+                              cudaStream_t stream);
+
 // ---- K2 (cuts.cu)
 struct VideoDesc {
   int64_t fbase;  // first frame in the batch's flat frame space

@@ -63,6 +63,10 @@ def _host_lib():
                                         ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32,
                                         ctypes.c_uint32, ctypes.c_void_p]
         lib.synth_pixel_ref.restype = None
+        lib.synth_gen_nv12.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                       ctypes.c_uint32, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        lib.synth_gen_nv12.restype = None
         _host = lib
     return _host
 
@@ -85,6 +89,10 @@ def dev_lib():
         lib.synth_dev_frame_hash.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                              ctypes.c_void_p, ctypes.c_void_p]
         lib.synth_dev_frame_hash.restype = ctypes.c_int
+        lib.synth_dev_gen_nv12.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.c_uint32, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.synth_dev_gen_nv12.restype = ctypes.c_int
         _dev = lib
     return _dev
 
@@ -106,6 +114,21 @@ def gen_frames(v: Video, t0: int = 0, n: int | None = None, nthreads: int | None
         nthreads = len(os.sched_getaffinity(0))
     fr = np.ascontiguousarray(v.frames)
     _host_lib().synth_gen_frames(v.seed, v.id, v.W, v.H, t0, n, _ptr(fr), _ptr(out), nthreads)
+    return out
+
+
+def gen_nv12(v: Video, t0: int = 0, n: int | None = None, nthreads: int | None = None,
+             out: np.ndarray | None = None) -> np.ndarray:
+    """Host NV12 frames t0..t0+n-1 of video ``v`` as u8 [n, H*3/2, W] (Y rows then UV rows)."""
+    if n is None:
+        n = v.n - t0
+    assert 0 <= t0 and t0 + n <= v.n and v.W % 2 == 0 and v.H % 2 == 0
+    if out is None:
+        out = np.empty((n, v.H * 3 // 2, v.W), dtype=np.uint8)
+    if nthreads is None:
+        nthreads = len(os.sched_getaffinity(0))
+    fr = np.ascontiguousarray(v.frames)
+    _host_lib().synth_gen_nv12(v.seed, v.id, v.W, v.H, t0, n, _ptr(fr), _ptr(out), nthreads)
     return out
 
 

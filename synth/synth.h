@@ -189,4 +189,75 @@ SYNTH_HD float synth_emb_value(int32_t dir, uint32_t key, uint32_t d) {
 /* ---- frame hash: fh = sum_i mix64(w_i ^ i) mod 2^64 over little-endian u64 words ---- */
 SYNTH_HD uint64_t synth_hash_word(uint64_t w, uint64_t i) { return synth_mix64(w ^ i); }
 
+
+/* ---- NV12 frames (NVDEC's native 4:2:0 output): a scene model in YUV.
+ * Y plane [H][W] then interleaved UV plane [H/2][W/2][2] (U then V).
+ * Palette colour k of a scene: Y in [16, 235], U, V in [16, 240]; luma noise +-6
+ * per pixel, chroma noise +-2 per 2x2 block.  Modes: 1 = chroma swapped (U,V) ->
+ * (V,U), 2 = chroma mirrored (256-U, 256-V) (both: "false cut", same scene);
+ * 3 = flash (Y = 235 - |noise|, U = V = 128); fade: Y -> 16 + w*(Y-16)/256,
+ * U,V -> 128 + w*(U-128)/256 (integer, rounded). */
+#define SYNTH_TAG_YUV 0x7A11E001ull
+
+SYNTH_HD uint32_t synth_yuv_palette(uint64_t seed, uint32_t video, uint32_t scene, uint32_t k,
+                                    uint32_t c) {
+  uint32_t h = (uint32_t)(synth_h5(seed ^ SYNTH_TAG_YUV, video, scene, k, c) & 0xFFFFu);
+  return c == 0 ? 16u + h % 220u : 16u + h % 225u;
+}
+
+SYNTH_HD uint32_t synth_fade8(uint32_t x, uint32_t center, uint32_t w) {
+  /* center + round(w*(x - center)/256), computed on non-negative integers */
+  int32_t d = (int32_t)x - (int32_t)center;
+  int32_t r = (d * (int32_t)w + 256 * 256 + 128) >> 8;  /* >= 0 for |d| <= 255 */
+  return (uint32_t)((int32_t)center + r - 256);
+}
+
+/* Luma of pixel (x, y). */
+SYNTH_HD uint32_t synth_nv12_y(uint64_t seed, uint32_t video, uint32_t t, synth_frame fr,
+                               uint32_t W, uint32_t x, uint32_t y) {
+  uint32_t cell = synth_cell(W);
+  uint32_t k = synth_cell_index(seed, video, fr.scene, x / cell + t / 8u, y / cell);
+  uint32_t word = synth_noise_word(synth_noise_key(seed, video, t), y * W + x);
+  int32_t n = synth_noise(word);
+  uint32_t Y;
+  if (fr.mode == SYNTH_MODE_NOISE) {
+    Y = word & 255u;
+  } else if (fr.mode == SYNTH_MODE_FLASH) {
+    Y = 235u - (uint32_t)(n < 0 ? -n : n);
+  } else {
+    Y = synth_clamp255((int32_t)synth_yuv_palette(seed, video, fr.scene, k, 0) + n);
+  }
+  if (fr.fade_w != 256u) Y = synth_fade8(Y, 16u, fr.fade_w);
+  return Y;
+}
+
+/* Chroma (U, V) of the 2x2 block (bx, by) = pixels (2bx.., 2by..). */
+SYNTH_HD void synth_nv12_uv(uint64_t seed, uint32_t video, uint32_t t, synth_frame fr, uint32_t W,
+                            uint32_t bx, uint32_t by, uint32_t* U, uint32_t* V) {
+  uint32_t cell = synth_cell(W);
+  uint32_t x = 2u * bx, y = 2u * by;
+  uint32_t k = synth_cell_index(seed, video, fr.scene, x / cell + t / 8u, y / cell);
+  uint32_t word = synth_noise_word(synth_noise_key(seed ^ SYNTH_TAG_YUV, video, t), by * W + bx);
+  int32_t n = (int32_t)((((word >> 16) * 5u) >> 16)) - 2; /* [-2, 2] */
+  uint32_t u = synth_clamp255((int32_t)synth_yuv_palette(seed, video, fr.scene, k, 1) + n);
+  uint32_t v = synth_clamp255((int32_t)synth_yuv_palette(seed, video, fr.scene, k, 2) - n);
+  if (fr.mode == SYNTH_MODE_NOISE) {
+    u = word & 255u;
+    v = (word >> 8) & 255u;
+  } else if (fr.mode == SYNTH_MODE_FLASH) {
+    u = 128u;
+    v = 128u;
+  } else if (fr.mode == SYNTH_MODE_ROT1) {
+    uint32_t tmp = u; u = v; v = tmp;
+  } else if (fr.mode == SYNTH_MODE_ROT2) {
+    u = 256u - u; v = 256u - v;
+  }
+  if (fr.fade_w != 256u) {
+    u = synth_fade8(u, 128u, fr.fade_w);
+    v = synth_fade8(v, 128u, fr.fade_w);
+  }
+  *U = u;
+  *V = v;
+}
+
 #endif /* SYNTH_H_ */

@@ -80,9 +80,48 @@ __global__ void frame_hash_kernel(const uint8_t* __restrict__ frames, int64_t by
   if ((threadIdx.x & 31) == 0) atomicAdd(out + f, acc);
 }
 
+// NV12: one thread per 2x2 block (4 luma + 1 chroma pair)
+__global__ void gen_nv12_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0,
+                                const synth_frame* __restrict__ frames, uint8_t* __restrict__ out) {
+  const int64_t f = blockIdx.y;
+  const uint32_t t = (uint32_t)(t0 + f);
+  const synth_frame fr = frames[t];
+  const uint32_t nb = (W / 2) * (H / 2);
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint32_t bx = b % (W / 2), by = b / (W / 2);
+  uint8_t* Y = out + (size_t)f * W * H * 3 / 2;
+  uint8_t* UV = Y + (size_t)W * H;
+  for (uint32_t dy = 0; dy < 2; ++dy)
+    for (uint32_t dx = 0; dx < 2; ++dx) {
+      const uint32_t x = 2 * bx + dx, y = 2 * by + dy;
+      Y[(size_t)y * W + x] = (uint8_t)synth_nv12_y(seed, video, t, fr, W, x, y);
+    }
+  uint32_t u, v;
+  synth_nv12_uv(seed, video, t, fr, W, bx, by, &u, &v);
+  UV[(size_t)by * W + 2 * bx] = (uint8_t)u;
+  UV[(size_t)by * W + 2 * bx + 1] = (uint8_t)v;
+}
+
 }  // namespace
 
 extern "C" {
+
+/* NV12 frames t0..t0+n-1 of one video into d_out ([n][H*W*3/2] u8, device). */
+int synth_dev_gen_nv12(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0,
+                       int64_t n, const synth_frame* d_frames, uint8_t* d_out, uintptr_t stream) {
+  if (n <= 0) return 0;
+  if ((W % 2) || (H % 2)) return (int)cudaErrorInvalidValue;
+  const uint32_t nb = (W / 2) * (H / 2);
+  for (int64_t f0 = 0; f0 < n; f0 += 65535) {
+    int64_t nf = n - f0 < 65535 ? n - f0 : 65535;
+    dim3 grid((nb + 255) / 256, (unsigned)nf);
+    gen_nv12_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, video, W, H, t0 + f0, d_frames,
+                                                            d_out + (size_t)f0 * W * H * 3 / 2);
+  }
+  return (int)cudaGetLastError();
+}
+
 
 /* Frames t0..t0+n-1 of one video into d_out ([n][H][W][3] u8, device).
  * d_frames: device array of synth_frame indexed by absolute frame index.

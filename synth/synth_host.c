@@ -89,6 +89,66 @@ void synth_gen_frames(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int
   for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
 }
 
+/* ---------------------------------------------------------------- NV12 */
+
+typedef struct {
+  uint64_t seed;
+  uint32_t video, W, H;
+  int64_t t0;
+  const synth_frame* frames;
+  uint8_t* out;
+  int64_t f_begin, f_end;
+} nv12_job;
+
+static void* nv12_worker(void* arg) {
+  nv12_job* j = (nv12_job*)arg;
+  const size_t fb = (size_t)j->W * j->H * 3 / 2;
+  for (int64_t f = j->f_begin; f < j->f_end; ++f) {
+    const uint32_t t = (uint32_t)(j->t0 + f);
+    const synth_frame fr = j->frames[t];
+    uint8_t* Y = j->out + (size_t)f * fb;
+    uint8_t* UV = Y + (size_t)j->W * j->H;
+    for (uint32_t y = 0; y < j->H; ++y)
+      for (uint32_t x = 0; x < j->W; ++x)
+        Y[(size_t)y * j->W + x] = (uint8_t)synth_nv12_y(j->seed, j->video, t, fr, j->W, x, y);
+    for (uint32_t by = 0; by < j->H / 2; ++by)
+      for (uint32_t bx = 0; bx < j->W / 2; ++bx) {
+        uint32_t u, v;
+        synth_nv12_uv(j->seed, j->video, t, fr, j->W, bx, by, &u, &v);
+        UV[(size_t)by * j->W + 2 * bx] = (uint8_t)u;
+        UV[(size_t)by * j->W + 2 * bx + 1] = (uint8_t)v;
+      }
+  }
+  return NULL;
+}
+
+/* NV12 frames t0..t0+n-1 (each: Y [H][W] then UV [H/2][W]) into out. */
+void synth_gen_nv12(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0, int64_t n,
+                    const synth_frame* frames, uint8_t* out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (nthreads > n) nthreads = (int)(n > 0 ? n : 1);
+  pthread_t th[256];
+  nv12_job jobs[256];
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i].seed = seed;
+    jobs[i].video = video;
+    jobs[i].W = W;
+    jobs[i].H = H;
+    jobs[i].t0 = t0;
+    jobs[i].frames = frames;
+    jobs[i].out = out;
+    jobs[i].f_begin = n * i / nthreads;
+    jobs[i].f_end = n * (i + 1) / nthreads;
+  }
+  if (nthreads == 1) {
+    nv12_worker(&jobs[0]);
+    return;
+  }
+  for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, nv12_worker, &jobs[i]);
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
 /* Uncached single pixel (for testing the memoised loop). */
 void synth_pixel_ref(uint64_t seed, uint32_t video, uint32_t t, const synth_frame* fr, uint32_t W,
                      uint32_t x, uint32_t y, uint8_t* out) {

@@ -34,6 +34,17 @@ def gen_frames(v: Video, table, out, t0: int = 0, n: int | None = None, stream=N
     return out
 
 
+def gen_nv12(v: Video, table, out, t0: int = 0, n: int | None = None, stream=None):
+    """NV12 frames t0..t0+n-1 of v into out (u8 cuda [n, H*3/2, W])."""
+    if n is None:
+        n = v.n - t0
+    rc = dev_lib().synth_dev_gen_nv12(v.seed, v.id, v.W, v.H, t0, n, table.data_ptr(),
+                                      out.data_ptr(), _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"synth_dev_gen_nv12 failed: cuda error {rc}")
+    return out
+
+
 def gen_emb(v: Video, table, out, t0: int = 0, n: int | None = None, stream=None):
     """Embeddings of frames t0..t0+n-1 into out (f32 cuda [n, D])."""
     if n is None:

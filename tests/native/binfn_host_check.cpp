@@ -64,12 +64,28 @@ int main(int argc, char** argv) {
         return 1;
       }
   }
+  // NV12 pair conversion + LUT codes for every (Y, U, V): lane 0 = Y, lane 1 = Y ^ 0x5A
+  std::vector<uint8_t> n0(N), n1(N);
+  for (uint32_t c = 0; c < N; ++c) {
+    const uint32_t Y = c >> 16, U = (c >> 8) & 255u, V = c & 255u, Y2 = Y ^ 0x5Au;
+    int32_t ruv, guv, buv;
+    nv12_chroma(U, V, ruv, guv, buv);
+    uint32_t R, G, B;
+    nv12_pair_rgb(Y, Y2, ruv, guv, buv, R, G, B);
+    uint32_t i0, i1;
+    const uint32_t pre = code_pair_lut_pre(R, G, B, kMadK, i0, i1);
+    const uint32_t lc = code_pair_lut_post(pre, lut[i0], lut[i1], kMadK);
+    n0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
+    n1[(Y2 << 16) | (U << 8) | V] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);
+  }
   FILE* f = fopen(argv[1], "wb");
   fwrite(t0.data(), 1, N, f);
   fwrite(t1.data(), 1, N, f);
   fwrite(tg.data(), 1, N, f);
   fwrite(l0.data(), 1, N, f);
   fwrite(l1.data(), 1, N, f);
+  fwrite(n0.data(), 1, N, f);
+  fwrite(n1.data(), 1, N, f);
   fclose(f);
   return 0;
 }

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
+from nv12_helpers import yuv_rgb_table
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "tests", "native", "binfn_host_check.cpp")
@@ -28,7 +29,7 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
     subprocess.check_call([exe, path, *map(str, bins)])
     raw = np.fromfile(path, dtype=np.uint8)
     n = 1 << 24
-    t0, t1, tg, l0, l1 = (raw[i * n:(i + 1) * n] for i in range(5))
+    t0, t1, tg, l0, l1, n0, n1 = (raw[i * n:(i + 1) * n] for i in range(7))
     p = oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2])
     want = oracle.bin_table(p)
     assert np.array_equal(tg, want)
@@ -37,3 +38,7 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
         assert np.array_equal(t1, want), np.nonzero(t1 != want)[0][:10]
         assert np.array_equal(l0, want), np.nonzero(l0 != want)[0][:10]
         assert np.array_equal(l1, want), np.nonzero(l1 != want)[0][:10]
+        yuv = want[yuv_rgb_table()]  # bin of every (Y, U, V): oracle O0 then O1
+        assert np.array_equal(n0, yuv), np.nonzero(n0 != yuv)[0][:10]
+        assert np.array_equal(n1, yuv), np.nonzero(n1 != yuv)[0][:10]
+

@@ -401,3 +401,41 @@ def test_tiny_and_cutless_videos(ctx, dev):
         assert list(r.detected) == list(ref.detected)
         assert list(r.final) == list(ref.final)
         assert r.rounds == ref.rounds
+
+
+def test_c2_full_through_per_step_api_in_chunks(ctx, dev):
+    """C2 at full size through the per-step entry points, streamed in ~1 GiB
+    chunks: clip_frame_scores (prev_hist carry) -> clip_cuts (device-resident
+    state, tail rule on the last chunk) -> clip_merge; every histogram and L1
+    value and both cut lists equal the oracle golden."""
+    g = _golden("C2")["videos"][0]
+    v = manifest.c2_video()
+    table = torch_dev.frame_table(v, dev)
+    emb = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+    torch_dev.gen_emb(v, table, emb)
+    chunk = 388
+    buf = torch.empty((chunk, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+    hist = torch.empty((v.n, 162), dtype=torch.int32, device=dev)
+    l1 = torch.empty(v.n, dtype=torch.int32, device=dev)
+    state = torch.zeros(4, dtype=torch.int64, device=dev)
+    cuts = torch.empty(v.n // 8 + 2, dtype=torch.int32, device=dev)
+    prev = None
+    for t0 in range(0, v.n, chunk):
+        m = min(chunk, v.n - t0)
+        fr = buf[:m]
+        torch_dev.gen_frames(v, table, fr, t0=t0, n=m)
+        ctx.frame_scores(fr, prev_hist=prev, hist=hist[t0:t0 + m], l1=l1[t0:t0 + m],
+                         want_score=False)
+        ctx.cuts(l1[t0:t0 + m], v.W * v.H, state, cuts, t0 + m == v.n)
+        prev = hist[t0 + m - 1]
+    torch.cuda.synchronize()
+    assert hashlib.sha256(_u32(hist).tobytes()).hexdigest() == g["hist_sha256"]
+    assert hashlib.sha256(_u32(l1).tobytes()).hexdigest() == g["l1_sha256"]
+    st = state.cpu().numpy()
+    assert st[2] == g["n_candidates"] and st[0] == v.n
+    det = cuts.cpu().numpy()[:st[3]].tolist()
+    assert det == g["detected"]
+    merged, cos, hits, rounds = ctx.merge(emb, cuts[:st[3]].contiguous(), n_cuts=int(st[3]))
+    assert merged.cpu().numpy().tolist() == g["final"]
+    np.testing.assert_allclose(cos.cpu().numpy(), np.array(g["cos"]), rtol=COS_RTOL, atol=1e-12)
+    assert hits == g["n_band_hits"] and rounds == g["rounds"]

@@ -11,7 +11,10 @@ C2-C5 (50 GB - 1.6 TB of frames) fit in host memory; the arithmetic is
 oracle.hist_frames / l1 / candidates / min_length / merge, i.e. oracle_video's
 steps in order.
 
-usage: python tools/make_goldens.py C1 [C2 ...] [--threads N] [--videos a:b]
+With --nv12 the frames are the generator's NV12 surfaces and the histogram
+is oracle.hist_nv12_frames (reading O0 then O2); written as <CONFIG>_NV12.json.
+
+usage: python tools/make_goldens.py C1 [C2 ...] [--threads N] [--nv12]
 """
 import argparse
 import hashlib
@@ -32,9 +35,9 @@ from synth import manifest  # noqa: E402
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 
 
-def golden_video(v, p, threads, chunk_bytes=2 << 30, buf=None):
+def golden_video(v, p, threads, chunk_bytes=2 << 30, buf=None, nv12=False):
     n = v.n
-    fb = v.frame_bytes
+    fb = v.npix * 3 // 2 if nv12 else v.frame_bytes
     chunk = max(1, min(n, chunk_bytes // fb))
     if buf is None or buf.size < chunk * fb:
         buf = np.empty(chunk * fb, dtype=np.uint8)
@@ -43,9 +46,14 @@ def golden_video(v, p, threads, chunk_bytes=2 << 30, buf=None):
     sample = sorted({0, n // 2, n - 1})
     for t0 in range(0, n, chunk):
         m = min(chunk, n - t0)
-        fr = buf[:m * fb].reshape(m, v.H, v.W, 3)
-        synth.gen_frames(v, t0=t0, n=m, nthreads=threads, out=fr)
-        hist[t0:t0 + m] = oracle.hist_frames(fr, p, nthreads=threads)
+        if nv12:
+            fr = buf[:m * fb].reshape(m, v.H * 3 // 2, v.W)
+            synth.gen_nv12(v, t0=t0, n=m, nthreads=threads, out=fr)
+            hist[t0:t0 + m] = oracle.hist_nv12_frames(fr, p, nthreads=threads)
+        else:
+            fr = buf[:m * fb].reshape(m, v.H, v.W, 3)
+            synth.gen_frames(v, t0=t0, n=m, nthreads=threads, out=fr)
+            hist[t0:t0 + m] = oracle.hist_frames(fr, p, nthreads=threads)
         for t in sample:
             if t0 <= t < t0 + m:
                 fh[str(t)] = str(synth.frame_hash(fr[t - t0]))
@@ -75,6 +83,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--threads", type=int, default=len(os.sched_getaffinity(0)))
+    ap.add_argument("--nv12", action="store_true")
     args = ap.parse_args()
     oracle.build()
     synth.build(device=False)
@@ -82,17 +91,17 @@ def main():
     for name in args.configs:
         t0 = time.time()
         vids = manifest.config_videos(name)
-        out = {"config": name, "params": p.__dict__, "emb_dim": manifest.EMB_DIM,
+        out = {"config": name, "format": "nv12" if args.nv12 else "rgb24", "params": p.__dict__, "emb_dim": manifest.EMB_DIM,
                "generator": "synth/synth.h + synth/manifest.py", "videos": []}
         buf = None
         for i, v in enumerate(vids):
-            rec, buf = golden_video(v, p, args.threads, buf=buf)
+            rec, buf = golden_video(v, p, args.threads, buf=buf, nv12=args.nv12)
             out["videos"].append(rec)
             if (i + 1) % max(1, len(vids) // 10) == 0:
                 print(f"{name}: {i + 1}/{len(vids)} videos, {time.time() - t0:.0f}s", flush=True)
         out["total_frames"] = int(sum(v.n for v in vids))
         out["seconds"] = round(time.time() - t0, 1)
-        path = os.path.join(GOLDEN_DIR, f"{name}.json")
+        path = os.path.join(GOLDEN_DIR, f"{name}_NV12.json" if args.nv12 else f"{name}.json")
         with open(path, "w") as f:
             json.dump(out, f, indent=0, separators=(",", ":"))
         print(f"wrote {path} in {time.time() - t0:.0f}s", flush=True)
