@@ -172,7 +172,9 @@ def run_ours(args):
     from synth import manifest, torch_dev
     from paper_2503_12964_b200 import Ctx
     from paper_2503_12964_b200 import dist as cdist
+    from paper_2503_12964_b200.clipdetect import FORMAT_NV12, FORMAT_RGB24
 
+    nv12 = args.format == "nv12"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -187,13 +189,19 @@ def run_ours(args):
     if args.frames:
         v = manifest.subsample(v, args.frames)
     table = torch_dev.frame_table(v, dev)
-    frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
-    torch_dev.gen_frames(v, table, frames)
+    if nv12:  # NEXT f1: the decoder's NV12 surfaces (reading O0), 1.5 B/px
+        frames = torch.empty((v.n, v.H * 3 // 2, v.W), dtype=torch.uint8, device=dev)
+        torch_dev.gen_nv12(v, table, frames)
+    else:
+        frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+        torch_dev.gen_frames(v, table, frames)
     emb = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
     torch_dev.gen_emb(v, table, emb)
     torch.cuda.synchronize()
-    frame_bytes = v.n * v.frame_bytes
-    item = [{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb, "id": v.id}]
+    fbytes = frames[0].numel()
+    frame_bytes = v.n * fbytes
+    fmt = FORMAT_NV12 if nv12 else FORMAT_RGB24
+    item = [{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb, "id": v.id, "format": fmt}]
 
     stream = torch.cuda.Stream(device=dev)
     ctx = Ctx(device=local, stream=stream, timing=True)
@@ -245,12 +253,13 @@ def run_ours(args):
     # ---- read ceiling of K1's TMA pipeline on the same frames (K6, no binning)
     read_gbs = None
     if not args.no_read_ceiling:
+        read_fn = ctx.debug_read_roofline_nv12 if nv12 else ctx.debug_read_roofline
         with torch.cuda.stream(stream):
-            ctx.debug_read_roofline(frames)
+            read_fn(frames)
             r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             r0.record(stream)
             for _ in range(3):
-                ctx.debug_read_roofline(frames)
+                read_fn(frames)
             r1.record(stream)
         torch.cuda.synchronize()
         read_gbs = frame_bytes / (r0.elapsed_time(r1) / 3 * 1e-3) / 1e9
@@ -258,7 +267,7 @@ def run_ours(args):
 
     # ---- parity of the timed results against the oracle golden (rank 0's video is C2 video 0)
     parity = None
-    gpath = os.path.join(ROOT, "tests", "golden", "C2.json")
+    gpath = os.path.join(ROOT, "tests", "golden", "C2_NV12.json" if nv12 else "C2.json")
     if rank == 0 and not args.frames and os.path.exists(gpath):
         g = json.load(open(gpath))["videos"][0]
         parity = (res.detected.tolist() == g["detected"] and res.final.tolist() == g["final"])
@@ -276,15 +285,16 @@ def run_ours(args):
         except Exception:
             avail = 64 << 30
         # pinned host copy of the video: at most ~35% of the free host RAM per rank
-        n_e2e = max(1, min(v.n, args.e2e_frames, int(0.35 * avail / max(1, world) / v.frame_bytes)))
-        host = torch.empty((n_e2e, v.H, v.W, 3), dtype=torch.uint8, pin_memory=True)
+        n_e2e = max(1, min(v.n, args.e2e_frames, int(0.35 * avail / max(1, world) / fbytes)))
+        host = torch.empty((n_e2e,) + tuple(frames.shape[1:]), dtype=torch.uint8, pin_memory=True)
         host.copy_(frames[:n_e2e])
         host_emb = torch.empty((n_e2e, manifest.EMB_DIM), dtype=torch.float32, pin_memory=True)
         host_emb.copy_(emb[:n_e2e])
         dev_emb = torch.empty_like(emb[:n_e2e])
         del frames
         torch.cuda.empty_cache()
-        item_h = [{"n": n_e2e, "H": v.H, "W": v.W, "frames": host.numpy(), "emb": dev_emb, "id": v.id}]
+        item_h = [{"n": n_e2e, "H": v.H, "W": v.W, "frames": host.numpy(), "emb": dev_emb, "id": v.id,
+                   "format": fmt}]
 
         def step_e2e():
             with torch.cuda.stream(stream):
@@ -309,7 +319,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(se["memcpy_h2d"] / ne + host_emb.numel() * 4),
                "d2h_bytes_per_step": int(se["memcpy_d2h"] / ne),
                "frames_per_step_per_gpu": n_e2e,
-               "note": "pinned host RGB24 frames + embeddings copied H2D inside the timed region "
+               "note": f"pinned host {'NV12' if nv12 else 'RGB24'} frames + embeddings copied H2D inside the timed region "
                        "(PCIe-bound); detected/final cut lists copied D2H"}
 
     if world > 1:
@@ -325,7 +335,7 @@ def run_ours(args):
     achieved = k1_alg / (k1_ms * 1e-3) / 1e9
     traffic = None
     instr_px = None
-    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "k1_nv12_traffic.json" if nv12 else "k1_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
@@ -349,17 +359,21 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": "C2: 10-min 720p 30fps synthetic video (18,000 frames, 49.8 GB RGB24) "
-                               "per GPU, resident in HBM (BASELINE.json configs[1])",
+        "config": {"workload": ("C2 as NV12 surfaces (18,000 720p frames, 24.9 GB NV12; NEXT f1, reading O0) "
+                                "per GPU, resident in HBM" if nv12 else
+                                "C2: 10-min 720p 30fps synthetic video (18,000 frames, 49.8 GB RGB24) "
+                                "per GPU, resident in HBM (BASELINE.json configs[1])"),
+                   "format": "nv12" if nv12 else "rgb24",
                    "frames_per_gpu": v.n, "resolution": f"{v.W}x{v.H}", "emb_dim": manifest.EMB_DIM,
-                   "l2": "inputs larger than L2 (49.8 GB per GPU vs 126 MB), no flush needed",
+                   "l2": f"inputs larger than L2 ({frame_bytes / 1e9:.1f} GB per GPU vs 126 MB), no flush needed",
                    "parallelism": f"whole-video sharding, {world} GPU(s), one NCCL all-gather of cut lists"},
         "hbm_gbs": round(gbs, 1),
         "frac_of_measured_hbm": round(gbs / peak, 4),
         "frac_of_8tbs": round(gbs / 8000.0, 4),
         "read_ceiling_gbs": None if read_gbs is None else round(read_gbs, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k1_hist_kernel",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "k1_nv12_kernel" if nv12 else "k1_hist_kernel",
                      "alg_bytes_per_launch": k1_alg, "launch_ms": round(k1_ms, 4), "peak_src": peak_src,
                      "frac_of_read_ceiling": None if read_gbs is None else round(achieved / read_gbs, 4),
                      "frac_of_8tbs": round(achieved / 8000.0, 4), "instr_per_px_ncu": instr_px},
@@ -610,6 +624,8 @@ def main():
     ap.add_argument("--no-gather", action="store_true", help="diagnosis: skip the result all-gather")
     ap.add_argument("--no-read-ceiling", action="store_true")
     ap.add_argument("--config", default="", help="C3|C4|C5: strong-scaling batch run")
+    ap.add_argument("--format", default="rgb24", choices=["rgb24", "nv12"],
+                    help="frame format of the C2 run (nv12 = NEXT f1, fused NV12 kernel)")
     ap.add_argument("--max-videos", type=int, default=0)
     ap.add_argument("--resident-gb", type=float, default=150.0)
     ap.add_argument("--shard-frames", action="store_true",
