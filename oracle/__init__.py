@@ -90,6 +90,9 @@ def lib():
                                             P, P, P]),
             "oracle_nv12_to_rgb": (None, [P, I64, I64, P]),
             "oracle_hist_nv12_frames": (None, [P, I64, I64, I64, I32, I32, I32, P, ctypes.c_int]),
+            "oracle_sample_index": (I64, [I64, I64, I64, I64]),
+            "oracle_resize_linear": (None, [P, I64, I64, P, I64, I64]),
+            "oracle_sample_clips": (None, [P, I64, I64, I64, P, I64, I64, I64, I64, P, P]),
         }
         for name, (res, args) in sigs.items():
             f = getattr(L, name)
@@ -268,3 +271,29 @@ def run_video(frames: np.ndarray, emb: np.ndarray | None, p: Params = Params(),
     return VideoResult(h, l1_, sc, int(res.n_candidates), det[:nd].copy(),
                        fin[:res.n_final].copy(), cos[:nd].copy(), int(res.n_band_hits),
                        int(res.rounds))
+
+
+# ---------------------------------------------------------------- O10/O11 (NEXT f3)
+def sample_index(s: int, e: int, i: int, k: int) -> int:
+    """O10: frame i of k sampled from clip [s, e)."""
+    return int(lib().oracle_sample_index(s, e, i, k))
+
+
+def resize_linear(frame: np.ndarray, H2: int, W2: int) -> np.ndarray:
+    """O11: one RGB24 frame [H, W, 3] -> [H2, W2, 3]."""
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    out = np.empty((H2, W2, 3), dtype=np.uint8)
+    lib().oracle_resize_linear(_p(f), f.shape[0], f.shape[1], _p(out), H2, W2)
+    return out
+
+
+def sample_clips(frames: np.ndarray, cuts, k: int, H2: int, W2: int) -> tuple:
+    """O10 + O11 for one video: (out u8 [(n_cuts+1)*k, H2, W2, 3], index i64 [(n_cuts+1)*k])."""
+    f = np.ascontiguousarray(frames, dtype=np.uint8)
+    c = np.ascontiguousarray(np.asarray(cuts, dtype=np.int64))
+    m = (c.size + 1) * k
+    out = np.empty((m, H2, W2, 3), dtype=np.uint8)
+    idx = np.empty(m, dtype=np.int64)
+    lib().oracle_sample_clips(_p(f), f.shape[0], f.shape[1], f.shape[2], _p(c) if c.size else None,
+                              c.size, k, H2, W2, _p(out), _p(idx))
+    return out, idx

@@ -371,3 +371,74 @@ int oracle_video(const uint8_t* frames, int64_t n, int64_t npix, const float* em
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------ O10/O11 (NEXT f3) */
+/* O10: frame i (0 <= i < k) sampled from clip [s, e): the middle of the i-th of
+ * k equal parts, s + floor((2i + 1)(e - s) / (2k)). */
+int64_t oracle_sample_index(int64_t s, int64_t e, int64_t i, int64_t k) {
+  return s + ((2 * i + 1) * (e - s)) / (2 * k);
+}
+
+/* O11 coefficients of one output coordinate d of an axis src -> dst: OpenCV's
+ * 8-bit INTER_LINEAR (half-pixel centres, float32 position, 11-bit weights
+ * rounded to nearest-even, clamped at the border). */
+static void lin_coeff(int64_t src, int64_t dst, int64_t d, int64_t* s0, int64_t* s1, int32_t* w0,
+                      int32_t* w1) {
+  const double scale = 1.0 / ((double)dst / (double)src);
+  float f = (float)(((double)d + 0.5) * scale - 0.5);
+  int64_t s = (int64_t)floorf(f);
+  f = f - (float)s;
+  if (s < 0) {
+    f = 0.0f;
+    s = 0;
+  }
+  if (s >= src - 1) {
+    f = 0.0f;
+    s = src - 1;
+  }
+  *s0 = s;
+  *s1 = s + 1 < src ? s + 1 : src - 1;
+  *w0 = (int32_t)lrintf((1.0f - f) * 2048.0f);
+  *w1 = (int32_t)lrintf(f * 2048.0f);
+}
+
+/* O11: resize one RGB24 frame [H][W][3] -> [H2][W2][3].  Horizontal pass
+ * h = p0*w0 + p1*w1 (exact int), vertical pass
+ * out = sat((((h0 >> 4) * v0 >> 16) + ((h1 >> 4) * v1 >> 16) + 2) >> 2)
+ * (the fixed-point rounding of OpenCV's vectorised 8-bit path). */
+void oracle_resize_linear(const uint8_t* src, int64_t H, int64_t W, uint8_t* dst, int64_t H2,
+                          int64_t W2) {
+  for (int64_t dy = 0; dy < H2; ++dy) {
+    int64_t y0, y1;
+    int32_t v0, v1;
+    lin_coeff(H, H2, dy, &y0, &y1, &v0, &v1);
+    for (int64_t dx = 0; dx < W2; ++dx) {
+      int64_t x0, x1;
+      int32_t w0, w1;
+      lin_coeff(W, W2, dx, &x0, &x1, &w0, &w1);
+      for (int c = 0; c < 3; ++c) {
+        const int64_t h0 = (int64_t)src[(y0 * W + x0) * 3 + c] * w0 + (int64_t)src[(y0 * W + x1) * 3 + c] * w1;
+        const int64_t h1 = (int64_t)src[(y1 * W + x0) * 3 + c] * w0 + (int64_t)src[(y1 * W + x1) * 3 + c] * w1;
+        const int64_t t0 = ((h0 >> 4) * v0) >> 16, t1 = ((h1 >> 4) * v1) >> 16;
+        const int64_t o = (t0 + t1 + 2) >> 2;
+        dst[(dy * W2 + dx) * 3 + c] = (uint8_t)(o < 0 ? 0 : (o > 255 ? 255 : o));
+      }
+    }
+  }
+}
+
+/* O10 + O11 for one video: clips from cuts[n_cuts] (O7), k frames per clip,
+ * out [(n_cuts+1)*k][H2][W2][3] in clip order, index [(n_cuts+1)*k]. */
+void oracle_sample_clips(const uint8_t* frames, int64_t n, int64_t H, int64_t W, const int64_t* cuts,
+                         int64_t n_cuts, int64_t k, int64_t H2, int64_t W2, uint8_t* out,
+                         int64_t* index) {
+  for (int64_t c = 0; c <= n_cuts; ++c) {
+    const int64_t s = c == 0 ? 0 : cuts[c - 1];
+    const int64_t e = c == n_cuts ? n : cuts[c];
+    for (int64_t i = 0; i < k; ++i) {
+      const int64_t t = oracle_sample_index(s, e, i, k);
+      index[c * k + i] = t;
+      oracle_resize_linear(frames + t * H * W * 3, H, W, out + (c * k + i) * H2 * W2 * 3, H2, W2);
+    }
+  }
+}

@@ -93,4 +93,18 @@ int oracle_video(const uint8_t* frames, int64_t n, int64_t npix, const float* em
                  double* score, int64_t* detected, int64_t* final_cuts, double* cos,
                  oracle_result* res);
 
+/* O10 (NEXT f3): frame i of k sampled from clip [s, e): s + floor((2i+1)(e-s) / (2k)). */
+int64_t oracle_sample_index(int64_t s, int64_t e, int64_t i, int64_t k);
+
+/* O11 (NEXT f3): bilinear resize of one RGB24 frame [H][W][3] -> [H2][W2][3]
+ * (OpenCV 8-bit INTER_LINEAR fixed point). */
+void oracle_resize_linear(const uint8_t* src, int64_t H, int64_t W, uint8_t* dst, int64_t H2,
+                          int64_t W2);
+
+/* O10 + O11 for one video's clips (cuts as in O7): out [(n_cuts+1)*k][H2][W2][3],
+ * index [(n_cuts+1)*k]. */
+void oracle_sample_clips(const uint8_t* frames, int64_t n, int64_t H, int64_t W, const int64_t* cuts,
+                         int64_t n_cuts, int64_t k, int64_t H2, int64_t W2, uint8_t* out,
+                         int64_t* index);
+
 #endif /* ORACLE_H_ */
