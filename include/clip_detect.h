@@ -146,6 +146,23 @@ int clip_merge(clip_ctx* ctx, const float* emb, int64_t n_frames, int32_t dim,
                const int32_t* cuts, int64_t n_cuts, int32_t* merged, int64_t* n_merged,
                double* boundary_cos, int64_t* n_band_hits, int32_t* rounds);
 
+/* Clip frame sampling + resize (NEXT f3, readings O10/O11) for ONE video: the
+ * step after the path, producing the encoder input of every final clip
+ * (the clips feed "video embeddings").
+ *   frames   device u8 [n_frames][height][width][3] (RGB24, as clip_frame_scores)
+ *   cuts     device i32 [n_cuts] final cuts, strictly increasing in (0, n_frames)
+ *            (clips [0,c0), [c0,c1), ..., [c_last, n_frames), as O7)
+ *   k        frames per clip (>= 1): frame i of clip [s, e) is
+ *            s + floor((2i+1)(e-s) / 2k)  (O10: middles of k equal parts)
+ *   out_h, out_w  output size (>= 1, out_w <= 4096)
+ *   out      device u8 [(n_cuts+1)*k][out_h][out_w][3], clip-major (O11: OpenCV
+ *            INTER_LINEAR 8-bit fixed point, computed on the device)
+ *   index    device i32 [(n_cuts+1)*k] out or NULL: the sampled frame indices
+ * Errors: CLIP_E_INVALID for bad sizes / NULL pointers.  Async. */
+int clip_sample_frames(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                       int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k, int32_t out_h,
+                       int32_t out_w, uint8_t* out, int32_t* index);
+
 /* ---------------------------------------------------------------- batch API */
 
 #define CLIP_FORMAT_RGB24 0 /* u8 [n][H][W][3]                */

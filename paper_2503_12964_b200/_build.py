@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libclipdetect.so")
-SOURCES = ["hist.cu", "hist_nv12.cu", "cuts.cu", "merge.cu", "api.cu"]
+SOURCES = ["hist.cu", "hist_nv12.cu", "cuts.cu", "merge.cu", "sample.cu", "api.cu"]
 HEADERS = ["common.cuh", "binfn.cuh", "kernels.cuh"]
 PUBLIC_HEADER = os.path.join(os.path.dirname(HERE), "include", "clip_detect.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

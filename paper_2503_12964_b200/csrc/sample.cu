@@ -1,0 +1,156 @@
+// sample.cu — K4: clip frame sampling + resize (NEXT f3; readings O10, O11).
+//
+// The step after the path (§2.1: the final clips feed "video
+// embeddings" and transcoding): for every final clip [s, e) of a video, take
+// k frames t_i = s + floor((2i+1)(e-s) / 2k) (O10) and resize each to the
+// encoder input H2 x W2 with OpenCV's 8-bit bilinear fixed point (O11):
+//   horizontal  h = p[x0]*a0 + p[x1]*a1               (11-bit weights)
+//   vertical    o = sat((((h0 >> 4)*b0 >> 16) + ((h1 >> 4)*b1 >> 16) + 2) >> 2)
+// with the weights of each output coordinate computed in-kernel exactly as
+// OpenCV does (double position, float fraction, round-to-nearest-even).
+//
+// B200 design: HBM-bound gather.  One CTA per (output frame, band of RB output
+// rows): one elected thread moves the band's 2*RB source rows HBM -> shared
+// memory with 1-D TMA bulk copies (16-byte-aligned supersets of the rows,
+// completion on one mbarrier, L2 evict-first); the x weights of the W2 output
+// columns are computed once per CTA into shared memory; the 256 threads then
+// produce the band's pixels from shared memory (3 channels per thread-pixel)
+// and store them (the output is ~8 % of the bytes read).  Many CTAs per SM
+// keep the copies of several bands in flight.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace clipdetect {
+
+namespace {
+
+constexpr int kK4Threads = 256;
+constexpr int kK4SmemRows = 40 * 1024;  // budget for the staged source rows per CTA
+constexpr int kK4MaxW2 = 4096;
+
+struct LinCoeff {
+  int32_t s0, s1;
+  int32_t w0, w1;
+};
+
+// O11 coefficients of output coordinate d on an axis src -> dst (OpenCV
+// INTER_LINEAR, 8-bit): identical IEEE operations on the device.
+__device__ __forceinline__ LinCoeff lin_coeff(int32_t src, int32_t dst, int32_t d) {
+  const double scale = 1.0 / ((double)dst / (double)src);
+  float f = __double2float_rn(((double)d + 0.5) * scale - 0.5);
+  int32_t s = (int32_t)floorf(f);
+  f = __fsub_rn(f, (float)s);
+  if (s < 0) {
+    f = 0.0f;
+    s = 0;
+  }
+  if (s >= src - 1) {
+    f = 0.0f;
+    s = src - 1;
+  }
+  LinCoeff c;
+  c.s0 = s;
+  c.s1 = s + 1 < src ? s + 1 : src - 1;
+  c.w0 = __float2int_rn(__fmul_rn(__fsub_rn(1.0f, f), 2048.0f));
+  c.w1 = __float2int_rn(__fmul_rn(f, 2048.0f));
+  return c;
+}
+
+__global__ void __launch_bounds__(kK4Threads)
+k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32_t W,
+                 const int32_t* __restrict__ cuts, int32_t n_cuts, int32_t k, int32_t H2, int32_t W2,
+                 int32_t rb, int32_t bands, int32_t slot_bytes, uint8_t* __restrict__ out,
+                 int32_t* __restrict__ index) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ int32_t row_off[64];  // per staged row: offset of the row's first byte in its slot
+  __shared__ LinCoeff ycs[32];     // y weights of the band's output rows
+  LinCoeff* xc = reinterpret_cast<LinCoeff*>(sm);                    // [W2]
+  uint8_t* rows = sm + ((sizeof(LinCoeff) * W2 + 127) & ~(size_t)127);  // [2*rb][slot_bytes]
+
+  const int32_t j = blockIdx.x / bands, band = blockIdx.x - j * bands;
+  const int32_t c = j / k, i = j - c * k;
+  const int64_t s = c == 0 ? 0 : cuts[c - 1];
+  const int64_t e = c == n_cuts ? n : cuts[c];
+  int64_t t = s + ((2 * (int64_t)i + 1) * (e - s)) / (2 * (int64_t)k);  // O10
+  t = t < 0 ? 0 : (t >= n ? n - 1 : t);
+  if (band == 0 && threadIdx.x == 0 && index) index[j] = (int32_t)t;
+
+  const int32_t r0 = band * rb, nr = min(rb, H2 - r0);
+  const int64_t row_bytes = 3 * (int64_t)W;
+  const uint8_t* fb = frames + t * (int64_t)H * row_bytes;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t pol = policy_evict_first();
+    for (int32_t q = 0; q < 2 * nr; ++q) {
+      const LinCoeff yc = lin_coeff(H, H2, r0 + (q >> 1));
+      if ((q & 1) == 0) ycs[q >> 1] = yc;
+      const uint8_t* row = fb + (int64_t)(q & 1 ? yc.s1 : yc.s0) * row_bytes;
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(row) + row_bytes + 15) & ~(uintptr_t)15;
+      row_off[q] = (int32_t)(reinterpret_cast<uintptr_t>(row) - a0);
+      mbar_expect_tx(&bar, (uint32_t)(a1 - a0));
+      bulk_g2s(rows + (int64_t)q * slot_bytes, reinterpret_cast<const uint8_t*>(a0),
+               (uint32_t)(a1 - a0), &bar, pol);
+    }
+    mbar_arrive(&bar);
+  }
+  for (int32_t dx = threadIdx.x; dx < W2; dx += blockDim.x) xc[dx] = lin_coeff(W, W2, dx);
+  __syncthreads();
+  mbar_wait(&bar, 0);
+
+  uint8_t* ob = out + ((int64_t)j * H2 + r0) * W2 * 3;
+  for (int32_t p = threadIdx.x; p < nr * W2; p += blockDim.x) {
+    const int32_t dy = p / W2, dx = p - dy * W2;
+    const LinCoeff yc = ycs[dy];
+    const LinCoeff x = xc[dx];
+    const uint8_t* q0 = rows + (int64_t)(2 * dy) * slot_bytes + row_off[2 * dy];
+    const uint8_t* q1 = rows + (int64_t)(2 * dy + 1) * slot_bytes + row_off[2 * dy + 1];
+    const int32_t o0 = 3 * x.s0, o1 = 3 * x.s1;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const int32_t h0 = q0[o0 + ch] * x.w0 + q0[o1 + ch] * x.w1;
+      const int32_t h1 = q1[o0 + ch] * x.w0 + q1[o1 + ch] * x.w1;
+      const int32_t v = ((((h0 >> 4) * yc.w0) >> 16) + (((h1 >> 4) * yc.w1) >> 16) + 2) >> 2;
+      ob[(int64_t)p * 3 + ch] = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+    }
+  }
+}
+
+}  // namespace
+
+int k4_rows_per_band(int32_t W) {
+  const int32_t slot = ((3 * W + 32) + 15) & ~15;
+  int32_t rb = kK4SmemRows / (2 * slot);
+  if (rb > 32) rb = 32;
+  return rb < 1 ? 1 : rb;
+}
+
+int k4_max_width() { return kK4MaxW2; }
+
+cudaError_t k4_sample_launch(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
+                             const int32_t* cuts, int32_t n_cuts, int32_t k, int32_t H2, int32_t W2,
+                             uint8_t* out, int32_t* index, cudaStream_t stream) {
+  const int32_t rb = k4_rows_per_band(W);
+  const int32_t slot = ((3 * W + 32) + 15) & ~15;
+  const int32_t bands = (H2 + rb - 1) / rb;
+  const size_t smem = ((sizeof(LinCoeff) * W2 + 127) & ~(size_t)127) + (size_t)2 * rb * slot;
+  cudaError_t e = cudaFuncSetAttribute(k4_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (int64_t)(n_cuts + 1) * k * bands;
+  if (blocks <= 0) return cudaSuccess;
+  if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
+  k4_sample_kernel<<<(unsigned)blocks, kK4Threads, smem, stream>>>(frames, n, H, W, cuts, n_cuts, k,
+                                                                   H2, W2, rb, bands, slot, out,
+                                                                   index);
+  return cudaGetLastError();
+}
+
+}  // namespace clipdetect
