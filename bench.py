@@ -265,6 +265,43 @@ def run_ours(args):
         read_gbs = frame_bytes / (r0.elapsed_time(r1) / 3 * 1e-3) / 1e9
         ctx.stats(reset=True)
 
+    # ---- NEXT f3: K4 frame sampling + resize of the final clips (k per clip, 224x224)
+    f3 = None
+    if args.sample_k > 0 and not nv12:
+        cuts_d = torch.from_numpy(res.final.astype(np.int32)).to(dev)
+        S = 224
+        with torch.cuda.stream(stream):
+            out_s = torch.empty(((cuts_d.numel() + 1) * args.sample_k, S, S, 3), dtype=torch.uint8, device=dev)
+            for _ in range(3):
+                ctx.sample_frames(frames, cuts_d, args.sample_k, S, S, out=out_s, want_index=False)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(10):
+                ctx.sample_frames(frames, cuts_d, args.sample_k, S, S, out=out_s, want_index=False)
+            s1.record(stream)
+        torch.cuda.synchronize()
+        k4_ms = s0.elapsed_time(s1) / 10
+        ctx.stats(reset=True)
+        # algorithmic bytes per output frame: the distinct source rows the bilinear taps
+        # touch (O11 row coordinates) + the output frame
+        def src_rows(src, dst):
+            sc = 1.0 / (dst / src)
+            rows = set()
+            for d in range(dst):
+                f = float(np.float32((d + 0.5) * sc - 0.5))
+                y = int(np.floor(f))
+                y = min(max(y, 0), src - 1)
+                rows.update({y, min(y + 1, src - 1)})
+            return len(rows)
+        m = out_s.shape[0]
+        alg = m * (src_rows(v.H, S) * 3 * v.W + S * S * 3)
+        f3 = {"kernel": "k4_sample_kernel", "clips": int(cuts_d.numel() + 1), "k": args.sample_k,
+              "out": f"{S}x{S}", "launch_ms": round(k4_ms, 4),
+              "frames_out_per_s": round(m / (k4_ms * 1e-3), 1),
+              "roofline": {"bound": "hbm", "achieved": round(alg / (k4_ms * 1e-3) / 1e9, 1),
+                           "unit": "GB/s", "alg_bytes_per_launch": alg}}
+        del out_s
+
     # ---- parity of the timed results against the oracle golden (rank 0's video is C2 video 0)
     parity = None
     gpath = os.path.join(ROOT, "tests", "golden", "C2_NV12.json" if nv12 else "C2.json")
@@ -388,6 +425,10 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
+    if f3 is not None:
+        f3["roofline"]["peak"] = peak
+        f3["roofline"]["frac"] = round(f3["roofline"]["achieved"] / peak, 4)
+        line["f3_sample"] = f3
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -624,6 +665,8 @@ def main():
     ap.add_argument("--no-gather", action="store_true", help="diagnosis: skip the result all-gather")
     ap.add_argument("--no-read-ceiling", action="store_true")
     ap.add_argument("--config", default="", help="C3|C4|C5: strong-scaling batch run")
+    ap.add_argument("--sample-k", type=int, default=8,
+                    help="NEXT f3: also time K4 (k frames per final clip -> 224x224); 0 = off")
     ap.add_argument("--format", default="rgb24", choices=["rgb24", "nv12"],
                     help="frame format of the C2 run (nv12 = NEXT f1, fused NV12 kernel)")
     ap.add_argument("--max-videos", type=int, default=0)
