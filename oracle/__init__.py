@@ -91,6 +91,10 @@ def lib():
             "oracle_nv12_to_rgb": (None, [P, I64, I64, P]),
             "oracle_hist_nv12_frames": (None, [P, I64, I64, I64, I32, I32, I32, P, ctypes.c_int]),
             "oracle_sample_index": (I64, [I64, I64, I64, I64]),
+            "oracle_distance": (F64, [P, P, I32, I64, I32]),
+            "oracle_distances": (None, [P, I64, I32, I64, I32, P]),
+            "oracle_candidates_f64": (I64, [P, I64, I64, P]),
+            "oracle_candidates_adaptive": (I64, [P, I64, I64, I64, I64, I64, P]),
             "oracle_resize_linear": (None, [P, I64, I64, P, I64, I64]),
             "oracle_sample_clips": (None, [P, I64, I64, I64, P, I64, I64, I64, I64, P, P]),
         }
@@ -297,3 +301,60 @@ def sample_clips(frames: np.ndarray, cuts, k: int, H2: int, W2: int) -> tuple:
     lib().oracle_sample_clips(_p(f), f.shape[0], f.shape[1], f.shape[2], _p(c) if c.size else None,
                               c.size, k, H2, W2, _p(out), _p(idx))
     return out, idx
+
+
+# ---------------------------------------------------------------- O3'/O4' (NEXT f4)
+DIST_L1, DIST_CHI2, DIST_BHATTACHARYYA, DIST_CORREL = 0, 1, 2, 3
+
+
+def distance(a: np.ndarray, b: np.ndarray, npix: int, kind: int) -> float:
+    """O3': f64 distance of two histograms (kind 1 chi-square, 2 Bhattacharyya, 3 1 - correlation)."""
+    x = np.ascontiguousarray(a, dtype=np.uint32)
+    y = np.ascontiguousarray(b, dtype=np.uint32)
+    return float(lib().oracle_distance(_p(x), _p(y), x.size, npix, kind))
+
+
+def distances(hist_: np.ndarray, npix: int, kind: int) -> np.ndarray:
+    h = np.ascontiguousarray(hist_, dtype=np.uint32)
+    d = np.empty(h.shape[0], dtype=np.float64)
+    lib().oracle_distances(_p(h), h.shape[0], h.shape[1], npix, kind, _p(d))
+    return d
+
+
+def candidates_f64(d: np.ndarray, p: Params = Params()) -> np.ndarray:
+    x = np.ascontiguousarray(d, dtype=np.float64)
+    out = np.empty(max(1, x.size), dtype=np.int64)
+    k = lib().oracle_candidates_f64(_p(x), x.size, p.tau_ppm, _p(out))
+    return out[:k].copy()
+
+
+def candidates_adaptive(l1_: np.ndarray, npix: int, w: int, ratio_ppm: int,
+                        p: Params = Params()) -> np.ndarray:
+    x = np.ascontiguousarray(l1_, dtype=np.uint32)
+    out = np.empty(max(1, x.size), dtype=np.int64)
+    k = lib().oracle_candidates_adaptive(_p(x), x.size, npix, p.tau_ppm, w, ratio_ppm, _p(out))
+    return out[:k].copy()
+
+
+def run_video_variant(frames: np.ndarray, emb: np.ndarray | None, p: Params = Params(),
+                      distance_kind: int = DIST_L1, adaptive_window: int = 0,
+                      adaptive_ratio_ppm: int = 3000000, nv12: bool = False,
+                      nthreads: int | None = None) -> VideoResult:
+    """The path with the f4 variants: O1/O2 (or O0 first for NV12), then O3 (L1)
+    or O3' (distance_kind), O4 / O4' / O4'' (adaptive_window > 0, on L1), O5-O9."""
+    h = hist_nv12_frames(frames, p, nthreads) if nv12 else hist_frames(frames, p, nthreads)
+    n = h.shape[0]
+    npix = (frames.shape[1] * 2 // 3) * frames.shape[2] if nv12 else frames[0].size // 3
+    l1_, sc = l1(h, npix)
+    if adaptive_window > 0:
+        cand = candidates_adaptive(l1_, npix, adaptive_window, adaptive_ratio_ppm, p)
+    elif distance_kind != DIST_L1:
+        sc = distances(h, npix, distance_kind)
+        cand = candidates_f64(sc, p)
+    else:
+        cand = candidates(l1_, npix, p)
+    det = min_length(cand, n, p.l_min)
+    if emb is None:
+        return VideoResult(h, l1_, sc, int(cand.size), det, det.copy(), np.zeros(det.size), 0, 0)
+    m = merge(emb, det, p)
+    return VideoResult(h, l1_, sc, int(cand.size), det, m.final, m.cos, m.n_band_hits, m.rounds)

@@ -442,3 +442,89 @@ void oracle_sample_clips(const uint8_t* frames, int64_t n, int64_t H, int64_t W,
     }
   }
 }
+
+/* ------------------------------------------------------------------ O3'/O4' (NEXT f4) */
+/* O3' distance between the histograms a (frame t-1) and b (frame t), f64,
+ * bins in ascending order, N = npix pixels each:
+ *   kind 1  chi-square   D = (1/2N) sum_{a+b>0} (a-b)^2 / (a+b)           in [0, 1]
+ *   kind 2  Bhattacharyya D = sqrt(max(0, 1 - sum sqrt(a*b) / N))         in [0, 1]
+ *   kind 3  correlation  D = 1 - r, r = (K S_ab - N^2) / sqrt((K S_aa - N^2)(K S_bb - N^2)),
+ *           K = nbins, S_xy = sum x*y (exact integers); r = 1 if both
+ *           denominators are 0, else 0 if one is                        in [0, 2] */
+double oracle_distance(const uint32_t* a, const uint32_t* b, int32_t nbins, int64_t npix,
+                       int32_t kind) {
+  if (kind == 1) {
+    double acc = 0.0;
+    for (int32_t i = 0; i < nbins; ++i) {
+      const int64_t s = (int64_t)a[i] + (int64_t)b[i];
+      if (s == 0) continue;
+      const int64_t d = (int64_t)a[i] - (int64_t)b[i];
+      acc = acc + (double)(d * d) / (double)s;
+    }
+    return acc / (double)(2 * npix);
+  }
+  if (kind == 2) {
+    double acc = 0.0;
+    for (int32_t i = 0; i < nbins; ++i) acc = acc + sqrt((double)a[i] * (double)b[i]);
+    const double x = 1.0 - acc / (double)npix;
+    return sqrt(x > 0.0 ? x : 0.0);
+  }
+  if (kind == 3) {
+    int64_t sab = 0, saa = 0, sbb = 0;
+    for (int32_t i = 0; i < nbins; ++i) {
+      sab += (int64_t)a[i] * (int64_t)b[i];
+      saa += (int64_t)a[i] * (int64_t)a[i];
+      sbb += (int64_t)b[i] * (int64_t)b[i];
+    }
+    const int64_t n2 = npix * npix;
+    const int64_t num = (int64_t)nbins * sab - n2;
+    const int64_t A = (int64_t)nbins * saa - n2, B = (int64_t)nbins * sbb - n2;
+    double r;
+    if (A == 0 && B == 0) r = 1.0;
+    else if (A == 0 || B == 0) r = 0.0;
+    else r = (double)num / sqrt((double)A * (double)B);
+    return 1.0 - r;
+  }
+  return -1.0;
+}
+
+/* O3' for n frames of one video: d[0] = 0, d[t] = distance(h_{t-1}, h_t). */
+void oracle_distances(const uint32_t* hist, int64_t n, int32_t nbins, int64_t npix, int32_t kind,
+                      double* d) {
+  if (n > 0) d[0] = 0.0;
+  for (int64_t t = 1; t < n; ++t)
+    d[t] = oracle_distance(hist + (t - 1) * nbins, hist + t * nbins, nbins, npix, kind);
+}
+
+/* O4' fixed threshold on an f64 distance: candidate <=> t >= 1 and d[t] >= tau_ppm / 1e6. */
+int64_t oracle_candidates_f64(const double* d, int64_t n, int64_t tau_ppm, int64_t* cand) {
+  const double tau = (double)tau_ppm / 1e6;
+  int64_t k = 0;
+  for (int64_t t = 1; t < n; ++t)
+    if (d[t] >= tau) cand[k++] = t;
+  return k;
+}
+
+/* O4'' adaptive threshold on L1 (exact integers): with the neighbours
+ * U_t = {u : 1 <= u <= n-1, 0 < |u - t| <= w} (m = |U_t|), candidate <=>
+ * t >= 1, m > 0, L1_t * m * 1e6 >= ratio_ppm * sum_{u in U_t} L1_u, and
+ * L1_t * 1e6 >= tau_ppm * 2N (the fixed rule as a floor). */
+int64_t oracle_candidates_adaptive(const uint32_t* l1, int64_t n, int64_t npix, int64_t tau_ppm,
+                                   int64_t w, int64_t ratio_ppm, int64_t* cand) {
+  int64_t k = 0;
+  for (int64_t t = 1; t < n; ++t) {
+    unsigned __int128 sum = 0;
+    int64_t m = 0;
+    for (int64_t u = t - w; u <= t + w; ++u) {
+      if (u < 1 || u > n - 1 || u == t) continue;
+      sum += l1[u];
+      ++m;
+    }
+    if (m == 0) continue;
+    const unsigned __int128 lhs = (unsigned __int128)l1[t] * (unsigned __int128)m * 1000000u;
+    const unsigned __int128 rhs = (unsigned __int128)ratio_ppm * sum;
+    const int floor_ok = (uint64_t)l1[t] * 1000000ull >= (uint64_t)tau_ppm * (uint64_t)(2 * npix);
+    if (lhs >= rhs && floor_ok) cand[k++] = t;
+  }
+  return k;
+}

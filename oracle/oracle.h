@@ -107,4 +107,18 @@ void oracle_sample_clips(const uint8_t* frames, int64_t n, int64_t H, int64_t W,
                          int64_t n_cuts, int64_t k, int64_t H2, int64_t W2, uint8_t* out,
                          int64_t* index);
 
+/* O3' (NEXT f4): f64 distance of histograms a (t-1), b (t): kind 1 chi-square,
+ * 2 Bhattacharyya, 3 one minus correlation (definitions in oracle.c). */
+double oracle_distance(const uint32_t* a, const uint32_t* b, int32_t nbins, int64_t npix,
+                       int32_t kind);
+void oracle_distances(const uint32_t* hist, int64_t n, int32_t nbins, int64_t npix, int32_t kind,
+                      double* d);
+
+/* O4' (NEXT f4): candidates t >= 1 with d[t] >= tau_ppm / 1e6. */
+int64_t oracle_candidates_f64(const double* d, int64_t n, int64_t tau_ppm, int64_t* cand);
+
+/* O4'' (NEXT f4): adaptive candidates on L1 (window w, ratio ratio_ppm / 1e6, floor tau_ppm). */
+int64_t oracle_candidates_adaptive(const uint32_t* l1, int64_t n, int64_t npix, int64_t tau_ppm,
+                                   int64_t w, int64_t ratio_ppm, int64_t* cand);
+
 #endif /* ORACLE_H_ */
