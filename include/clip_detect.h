@@ -1,5 +1,5 @@
 /*
- * clip_detect.h — C ABI of libclipdetect (B200 / sm_100a), ABI version 1.
+ * clip_detect.h — C ABI of libclipdetect (B200 / sm_100a), ABI version 2.
  *
  * The hot path of the NeMo Curator clipping pipeline, PAPER.md:35 (§2.1
  * "Clipping Pipeline"): "It uses an aggressive method of splitting clips,
@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define CLIP_ABI_VERSION 1u
+#define CLIP_ABI_VERSION 2u
 
 typedef enum {
   CLIP_OK = 0,
@@ -71,7 +71,22 @@ typedef struct {
   double band_rel;            /* band hit iff |cos - theta| <= band_rel*theta (1e-5)  */
   uint32_t flags;             /* CLIP_FLAG_*                                          */
   uint32_t reserved;          /* must be 0                                            */
+  /* ABI 2: the f4 variants (readings O3', O4'' in DESIGN.md).
+   * Supported by clip_frame_scores (score) and clip_run_videos; clip_cuts
+   * (streaming on L1 values) accepts only the defaults (CLIP_E_INVALID otherwise). */
+  uint32_t distance;          /* O3': CLIP_DIST_* (default L1/TV); non-L1 distances are
+                                 f64, cut iff d >= cut_threshold_ppm / 1e6               */
+  uint32_t adaptive_window;   /* O4'': 0 = fixed threshold (default); w in [1, 1024]:
+                                 cut iff L1_t * m >= ratio * (sum of the m neighbour L1 within
+                                 +-w frames of the same video, frames >= 1) and the fixed
+                                 rule holds; needs distance = CLIP_DIST_L1                 */
+  uint64_t adaptive_ratio_ppm;/* O4'': ratio in ppm (3.0 = 3000000), <= 1e9              */
 } clip_params;
+
+#define CLIP_DIST_L1 0u            /* O3: L1 = 2N * total variation (exact integers) */
+#define CLIP_DIST_CHI2 1u          /* O3': (1/2N) sum (a-b)^2/(a+b)                  */
+#define CLIP_DIST_BHATTACHARYYA 2u /* O3': sqrt(1 - sum sqrt(a b) / N)               */
+#define CLIP_DIST_CORREL 3u        /* O3': 1 - Pearson correlation of the two histograms */
 
 typedef struct clip_ctx clip_ctx; /* opaque; one per device; not thread-safe */
 
@@ -95,7 +110,8 @@ const char* clip_last_error(const clip_ctx* ctx);
  *             chunk, or NULL at video start (then l1[0] = 0, reading O3)
  *   hist      device u32 [n_frames][nbins] out (O2: per-frame bin counts)
  *   l1        device u32 [n_frames] out or NULL (O3: sum_b |h_t - h_{t-1}|)
- *   score     device f32 [n_frames] out or NULL (O3: l1 / (2*H*W), f64 division rounded to f32)
+ *   score     device f32 [n_frames] out or NULL (O3: l1 / (2*H*W), f64 division rounded to f32;
+ *             with params.distance != L1 the O3' distance to the previous frame, f64 rounded to f32)
  * nbins = h_bins*s_bins*v_bins.  Async. */
 int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
                       int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,

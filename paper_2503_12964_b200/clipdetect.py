@@ -19,7 +19,8 @@ LIB_PATH = _build.LIB
 
 OK, E_INVALID, E_CAPACITY, E_CUDA, E_NOMEM, E_ARCH, E_STATE = range(7)
 FLAG_TIMING = 1
-ABI_VERSION = 1
+ABI_VERSION = 2
+DIST_L1, DIST_CHI2, DIST_BHATTACHARYYA, DIST_CORREL = 0, 1, 2, 3  # clip_params.distance (f4)
 
 
 class ClipError(RuntimeError):
@@ -34,7 +35,8 @@ class ClipParams(ctypes.Structure):
                 ("cut_threshold_ppm", ctypes.c_uint64), ("min_clip_frames", ctypes.c_uint32),
                 ("max_merge_rounds", ctypes.c_uint32), ("merge_cos_threshold", ctypes.c_double),
                 ("band_rel", ctypes.c_double), ("flags", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("reserved", ctypes.c_uint32), ("distance", ctypes.c_uint32),
+                ("adaptive_window", ctypes.c_uint32), ("adaptive_ratio_ppm", ctypes.c_uint64)]
 
 
 class ClipVideo(ctypes.Structure):

@@ -42,7 +42,7 @@ struct clip_ctx {
   std::string err;
   clip_stats stats{};
   // scratch
-  DevBuf segs, segs2, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
+  DevBuf segs, segs2, flags, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
       detcos, pack, pack_cos, sink;
   DevBuf m_video, m_clip_video, m_f0, m_f1, m_piece_base, m_P, m_S, m_alive, m_alive2, m_cos_b,
       m_cos_clip, m_counters, m_vstate, m_valive;
@@ -266,6 +266,11 @@ int validate_params(clip_ctx* ctx, const clip_params* p) {
     return fail(ctx, CLIP_E_INVALID, "merge_cos_threshold outside [-1, 1]");
   if (!(p->band_rel >= 0.0)) return fail(ctx, CLIP_E_INVALID, "band_rel < 0");
   if (p->reserved != 0) return fail(ctx, CLIP_E_INVALID, "reserved must be 0");
+  if (p->distance > CLIP_DIST_CORREL) return fail(ctx, CLIP_E_INVALID, "unknown distance %u", p->distance);
+  if (p->adaptive_window > 1024) return fail(ctx, CLIP_E_INVALID, "adaptive_window > 1024");
+  if (p->adaptive_window > 0 && p->distance != CLIP_DIST_L1)
+    return fail(ctx, CLIP_E_INVALID, "the adaptive threshold is defined on L1 (distance must be L1)");
+  if (p->adaptive_ratio_ppm > 1000000000ull) return fail(ctx, CLIP_E_INVALID, "adaptive_ratio_ppm > 1e9");
   return CLIP_OK;
 }
 
@@ -417,6 +422,9 @@ void clip_params_default(clip_params* p) {
   p->merge_cos_threshold = 0.90;
   p->band_rel = 1e-5;
   p->flags = 0;
+  p->distance = CLIP_DIST_L1;
+  p->adaptive_window = 0;
+  p->adaptive_ratio_ppm = 3000000;
 }
 
 int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uintptr_t cuda_stream) {
@@ -459,7 +467,7 @@ int clip_detect_destroy(clip_ctx* ctx) {
   if (!ctx) return CLIP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  DevBuf* bufs[] = {&ctx->segs, &ctx->segs2, &ctx->vids, &ctx->hist, &ctx->l1, &ctx->cand_slots,
+  DevBuf* bufs[] = {&ctx->segs, &ctx->segs2, &ctx->flags, &ctx->vids, &ctx->hist, &ctx->l1, &ctx->cand_slots,
                     &ctx->cand_count, &ctx->cuts, &ctx->ncuts, &ctx->ncand, &ctx->final_cuts,
                     &ctx->nfinal, &ctx->detcos, &ctx->pack, &ctx->pack_cos, &ctx->sink,
                     &ctx->m_video, &ctx->m_clip_video, &ctx->m_f0, &ctx->m_f1,
@@ -510,10 +518,18 @@ int frame_scores(clip_ctx* ctx, int format, const uint8_t* frames, int64_t n_fra
     CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
     CK(cudaMemcpyAsync(ctx->vids.p, &vd, sizeof vd, cudaMemcpyHostToDevice, ctx->stream));
     Span sp(ctx, 1);
-    CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1, score,
-                    ctx->p.cut_threshold_ppm, nullptr, nullptr, ctx->stream));
-    sp.end();
+    const bool var = ctx->p.distance != CLIP_DIST_L1;
+    CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1,
+                    var ? nullptr : score, ctx->p.cut_threshold_ppm, nullptr, nullptr, ctx->stream));
     ctx->stats.launches += 1;
+    if (var && score) {
+      int nl = 0;
+      CK(k2_variant_launch(hist, l1, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist,
+                           (int)ctx->p.distance, 0, 0, ctx->p.cut_threshold_ppm, score, nullptr,
+                           nullptr, nullptr, &nl, ctx->stream));
+      ctx->stats.launches += nl;
+    }
+    sp.end();
   }
   return CLIP_OK;
 }
@@ -542,6 +558,8 @@ int clip_cuts(clip_ctx* ctx, const uint32_t* l1, int64_t n_frames, int64_t pixel
   if (n_frames > 0 && !l1) return fail(ctx, CLIP_E_INVALID, "l1 is NULL");
   if (!state) return fail(ctx, CLIP_E_INVALID, "state is NULL");
   if (pixels_per_frame < 1) return fail(ctx, CLIP_E_INVALID, "pixels_per_frame < 1");
+  if (ctx->p.distance != CLIP_DIST_L1 || ctx->p.adaptive_window > 0)
+    return fail(ctx, CLIP_E_INVALID, "clip_cuts streams the default L1 rule only (use clip_run_videos for variants)");
   if (cuts_capacity < 0 || (cuts_capacity > 0 && !cuts))
     return fail(ctx, CLIP_E_INVALID, "bad cuts buffer");
   const int64_t blocks = (n_frames + kCompactFrames - 1) / kCompactFrames;
@@ -727,9 +745,20 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
   // ---- K2: distance, threshold, ordered compaction, greedy + tail
   {
     Span sp(ctx, 1);
+    const bool var = ctx->p.distance != CLIP_DIST_L1 || ctx->p.adaptive_window > 0;
     CK(k2_l1_launch(d_hist, F, P<VideoDesc>(ctx->vids), n_videos, nbins, nullptr, d_l1, nullptr,
-                    ctx->p.cut_threshold_ppm, P<int32_t>(ctx->cand_slots),
+                    ctx->p.cut_threshold_ppm, var ? nullptr : P<int32_t>(ctx->cand_slots),
                     P<int32_t>(ctx->cand_count), ctx->stream));
+    if (var) {
+      CKS(ensure(ctx, ctx->flags, F));
+      int nl = 0;
+      CK(k2_variant_launch(d_hist, d_l1, F, P<VideoDesc>(ctx->vids), n_videos, nbins, nullptr,
+                           (int)ctx->p.distance, (int32_t)ctx->p.adaptive_window,
+                           ctx->p.adaptive_ratio_ppm, ctx->p.cut_threshold_ppm, nullptr,
+                           P<uint8_t>(ctx->flags), P<int32_t>(ctx->cand_slots),
+                           P<int32_t>(ctx->cand_count), &nl, ctx->stream));
+      ctx->stats.launches += nl;
+    }
     CK(k2_greedy_launch(P<VideoDesc>(ctx->vids), n_videos, P<int32_t>(ctx->cand_slots),
                         P<int32_t>(ctx->cand_count), L, P<int32_t>(ctx->cuts),
                         P<int32_t>(ctx->ncuts), P<int32_t>(ctx->ncand), ctx->stream));

@@ -207,6 +207,104 @@ __global__ void k2_stream_greedy_kernel(int64_t n, int64_t l_min, CutState* __re
   }
 }
 
+// ------------------------------------------------------------ f4 variants
+// O3' distances, one thread per frame, bins in ascending order, f64 with
+// explicitly rounded operations (no contraction): the same IEEE operations,
+// in the same order, as the oracle's plain loop, so the scores and every
+// threshold decision are bit-identical to it.
+__device__ double frame_distance(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                 uint32_t nbins, int64_t npix, int kind) {
+  if (kind == 1) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < nbins; ++i) {
+      const int64_t x = a[i], y = b[i];
+      const int64_t s = x + y;
+      if (s == 0) continue;
+      const int64_t d = x - y;
+      acc = __dadd_rn(acc, __ddiv_rn((double)(d * d), (double)s));
+    }
+    return __ddiv_rn(acc, (double)(2 * npix));
+  }
+  if (kind == 2) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < nbins; ++i)
+      acc = __dadd_rn(acc, __dsqrt_rn(__dmul_rn((double)a[i], (double)b[i])));
+    const double x = __dsub_rn(1.0, __ddiv_rn(acc, (double)npix));
+    return __dsqrt_rn(x > 0.0 ? x : 0.0);
+  }
+  int64_t sab = 0, saa = 0, sbb = 0;
+  for (uint32_t i = 0; i < nbins; ++i) {
+    const int64_t x = a[i], y = b[i];
+    sab += x * y;
+    saa += x * x;
+    sbb += y * y;
+  }
+  const int64_t n2 = npix * npix;
+  const int64_t num = (int64_t)nbins * sab - n2;
+  const int64_t A = (int64_t)nbins * saa - n2, B = (int64_t)nbins * sbb - n2;
+  double r;
+  if (A == 0 && B == 0) r = 1.0;
+  else if (A == 0 || B == 0) r = 0.0;
+  else r = __ddiv_rn((double)num, __dsqrt_rn(__dmul_rn((double)A, (double)B)));
+  return __dsub_rn(1.0, r);
+}
+
+// O3' scores (f32 out) and, unless adaptive, O4' flags d >= tau_ppm / 1e6.
+__global__ void __launch_bounds__(128)
+k2_dist_kernel(const uint32_t* __restrict__ hist, int64_t F, const VideoDesc* __restrict__ vids,
+               int32_t nvid, uint32_t nbins, const uint32_t* __restrict__ prev_hist, int kind,
+               uint64_t tau_ppm, float* __restrict__ score, uint8_t* __restrict__ flags) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const VideoDesc vd = vids[find_video(vids, nvid, f)];
+  const int64_t t = f - vd.fbase;
+  const uint32_t* cur = hist + f * nbins;
+  const uint32_t* prev = t >= 1 ? cur - nbins : prev_hist;
+  const double d = prev ? frame_distance(prev, cur, nbins, vd.npix, kind) : 0.0;
+  if (score) score[f] = __double2float_rn(d);
+  if (flags) flags[f] = t >= 1 && d >= __ddiv_rn((double)tau_ppm, 1e6);
+}
+
+// O4'' adaptive flags on L1 (exact integers, 128-bit products).
+__global__ void __launch_bounds__(128)
+k2_adaptive_kernel(const uint32_t* __restrict__ l1, int64_t F, const VideoDesc* __restrict__ vids,
+                   int32_t nvid, uint64_t tau_ppm, int32_t w, uint64_t ratio_ppm,
+                   uint8_t* __restrict__ flags) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const VideoDesc vd = vids[find_video(vids, nvid, f)];
+  const int64_t t = f - vd.fbase, n = vd.n;
+  bool c = false;
+  if (t >= 1) {
+    unsigned __int128 sum = 0;
+    int64_t m = 0;
+    for (int64_t u = t - w; u <= t + w; ++u) {
+      if (u < 1 || u > n - 1 || u == t) continue;
+      sum += l1[vd.fbase + u];
+      ++m;
+    }
+    const uint32_t x = l1[f];
+    if (m > 0) {
+      const unsigned __int128 lhs = (unsigned __int128)x * (unsigned __int128)m * 1000000u;
+      c = lhs >= (unsigned __int128)ratio_ppm * sum &&
+          (uint64_t)x * 1000000ull >= tau_ppm * (uint64_t)(2 * vd.npix);
+    }
+  }
+  flags[f] = c;
+}
+
+__global__ void __launch_bounds__(kCompactFrames)
+k2_compact_kernel(const uint8_t* __restrict__ flags, int64_t F, int32_t* __restrict__ cand_slots,
+                  int32_t* __restrict__ cand_count) {
+  __shared__ uint8_t sflag[kCompactFrames];
+  __shared__ int wcnt[kCompactFrames / 32];
+  const int64_t f = (int64_t)blockIdx.x * kCompactFrames + threadIdx.x;
+  sflag[threadIdx.x] = f < F ? flags[f] : 0;
+  __syncthreads();
+  compact_block(sflag, wcnt, blockIdx.x, (int32_t)((int64_t)blockIdx.x * kCompactFrames),
+                cand_slots, cand_count);
+}
+
 }  // namespace
 
 cudaError_t k2_l1_launch(const uint32_t* hist, int64_t F, const VideoDesc* d_vids, int32_t nvid,
@@ -217,6 +315,33 @@ cudaError_t k2_l1_launch(const uint32_t* hist, int64_t F, const VideoDesc* d_vid
   const int64_t blocks = (F + kCompactFrames - 1) / kCompactFrames;
   k2_l1_kernel<<<(unsigned)blocks, kL1Warps * 32, 0, stream>>>(
       hist, F, d_vids, nvid, nbins, prev_hist, l1, score, tau_ppm, cand_slots, cand_count);
+  return cudaGetLastError();
+}
+
+cudaError_t k2_variant_launch(const uint32_t* hist, const uint32_t* l1, int64_t F,
+                              const VideoDesc* d_vids, int32_t nvid, uint32_t nbins,
+                              const uint32_t* prev_hist, int kind, int32_t adaptive_w,
+                              uint64_t ratio_ppm, uint64_t tau_ppm, float* score, uint8_t* flags,
+                              int32_t* cand_slots, int32_t* cand_count, int* launches,
+                              cudaStream_t stream) {
+  if (F <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((F + 127) / 128);
+  *launches = 0;
+  if (kind != 0) {
+    k2_dist_kernel<<<blocks, 128, 0, stream>>>(hist, F, d_vids, nvid, nbins, prev_hist, kind,
+                                               tau_ppm, score, adaptive_w > 0 ? nullptr : flags);
+    ++*launches;
+  }
+  if (adaptive_w > 0 && flags) {
+    k2_adaptive_kernel<<<blocks, 128, 0, stream>>>(l1, F, d_vids, nvid, tau_ppm, adaptive_w,
+                                                   ratio_ppm, flags);
+    ++*launches;
+  }
+  if (cand_slots && flags) {
+    k2_compact_kernel<<<(unsigned)((F + kCompactFrames - 1) / kCompactFrames), kCompactFrames, 0,
+                        stream>>>(flags, F, cand_slots, cand_count);
+    ++*launches;
+  }
   return cudaGetLastError();
 }
 

@@ -56,6 +56,15 @@ cudaError_t k2_l1_launch(const uint32_t* hist, int64_t F, const VideoDesc* d_vid
                          uint32_t nbins, const uint32_t* prev_hist, uint32_t* l1, float* score,
                          uint64_t tau_ppm, int32_t* cand_slots, int32_t* cand_count,
                          cudaStream_t stream);
+// f4 variants: O3' distances (kind 1 chi-square, 2 Bhattacharyya, 3 1 - correlation;
+// f32 scores; flags d >= tau unless adaptive) and / or O4'' adaptive flags on L1
+// (adaptive_w > 0), then ordered compaction of the flags.
+cudaError_t k2_variant_launch(const uint32_t* hist, const uint32_t* l1, int64_t F,
+                              const VideoDesc* d_vids, int32_t nvid, uint32_t nbins,
+                              const uint32_t* prev_hist, int kind, int32_t adaptive_w,
+                              uint64_t ratio_ppm, uint64_t tau_ppm, float* score, uint8_t* flags,
+                              int32_t* cand_slots, int32_t* cand_count, int* launches,
+                              cudaStream_t stream);
 // greedy min-length + tail per video (one warp per video) over the compacted candidates.
 cudaError_t k2_greedy_launch(const VideoDesc* d_vids, int32_t nvid, const int32_t* cand_slots,
                              const int32_t* cand_count, int64_t l_min, int32_t* cuts,

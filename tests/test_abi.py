@@ -74,3 +74,30 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "oracle.h" not in text and "liboracle" not in text, f
+
+
+def test_ctypes_struct_layouts_match_the_header(tmp_path):
+    """Every struct the binding marshals has the header's size and field
+    offsets (compiled with the system C compiler against include/clip_detect.h)."""
+    from paper_2503_12964_b200 import clipdetect as cd
+    structs = {"clip_params": cd.ClipParams, "clip_video": cd.ClipVideo,
+               "clip_video_result": cd.ClipVideoResult, "clip_run_outputs": cd.ClipRunOutputs,
+               "clip_stats": cd.ClipStats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void) {']
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append('  return 0; }')
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-o", str(exe), str(src)])
+    got = {}
+    for line in subprocess.check_output([str(exe)], text=True).splitlines():
+        c, f, v = line.split()
+        got[(c, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
