@@ -18,4 +18,6 @@ if [ -n "$NCU" ]; then
   $P > gpurun_out/plain2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_hist -s 1 -c 1 -o gpurun_out/k1_full $P > gpurun_out/ncu_full.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k4_sample -s 1 -c 1 -o gpurun_out/k4_full $P > gpurun_out/ncu_k4.log 2>&1
+  echo "ncu rc=$?" >> gpurun_out/ncu_k4.log
 fi

@@ -71,6 +71,18 @@ __device__ __forceinline__ float ffma(float a, float b, float c) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t madwide_hi(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t r;
+  asm volatile("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return (uint32_t)(r >> 32);
+}
+__device__ __forceinline__ uint32_t viaddmnmx(uint32_t a, uint32_t b, uint32_t c) {
+  return (uint32_t)__viaddmin_s32_relu((int)a, (int)b, (int)c);
+}
+__device__ __forceinline__ uint32_t vmin_s16_relu(uint32_t a, uint32_t b) {
+  return __vimin_s16x2_relu(a, b);
+}
+
 template <int OP>
 __global__ void bench(uint32_t* out, int iters, uint32_t k1, uint32_t k2, long long* clk) {
   uint32_t x[8];
@@ -102,6 +114,12 @@ __global__ void bench(uint32_t* out, int iters, uint32_t k1, uint32_t k2, long l
       if (OP == 15) x[i] = iadd3(x[i], k1, k2 + (uint32_t)i);
       if (OP == 16) x[i] = vmax2(x[i], k1 + (uint32_t)i) ^ k2;
       if (OP == 17) x[i] = mulhi(x[i], k1 + (uint32_t)i);
+      if (OP == 18) x[i] = madwide_hi(x[i], k1 + (uint32_t)i, (uint64_t)k2 << 12);
+      if (OP == 19) x[i] = viaddmnmx(x[i], k1, k2 + (uint32_t)i);
+      if (OP == 20) x[i] = vmin_s16_relu(x[i], k1 + (uint32_t)i);
+      if (OP == 21) {  // mixed: IMAD.WIDE + PRMT
+        if (i & 1) x[i] = prmt(x[i], k1, 0x3210 ^ k2); else x[i] = madwide_hi(x[i], k1 + (uint32_t)i, (uint64_t)k2 << 12);
+      }
       if (OP == 10) {  // mixed: 1/3 lop3, 1/3 mad, 1/3 prmt
         if (i % 3 == 0) x[i] = lop3(x[i], k1, k2);
         else if (i % 3 == 1) x[i] = mad(x[i], k1, k2);
@@ -166,6 +184,10 @@ int main() {
     run<15>("IADD3-3op", bps, 256);
     run<16>("VIMNMX.U16x2+LOP3", bps, 256);
     run<17>("IMAD.HI", bps, 256);
+    run<18>("IMAD.WIDE(hi)", bps, 256);
+    run<19>("VIADDMNMX.RELU", bps, 256);
+    run<20>("VIMNMX.S16x2.RELU", bps, 256);
+    run<21>("IMAD.WIDE+PRMT", bps, 256);
   }
   return 0;
 }
