@@ -86,6 +86,7 @@ def lib():
             "oracle_clip_sum": (None, [P, I64, I64, I64, P]),
             "oracle_cosine": (F64, [P, P, I64]),
             "oracle_merge": (I64, [P, I64, I64, P, I64, F64, F64, I32, P, P, P, P]),
+            "oracle_merge_stride": (I64, [P, I64, I64, P, I64, F64, F64, I32, I64, P, P, P, P]),
             "oracle_video": (ctypes.c_int, [P, I64, I64, P, I64, P, ctypes.c_int, P, P, P, P,
                                             P, P, P]),
             "oracle_nv12_to_rgb": (None, [P, I64, I64, P]),
@@ -227,7 +228,8 @@ class MergeResult:
     rounds: int
 
 
-def merge(emb: np.ndarray, cuts, p: Params = Params()) -> MergeResult:
+def merge(emb: np.ndarray, cuts, p: Params = Params(), stride: int = 1) -> MergeResult:
+    """O8 + O9 (stride > 1: O8' keyframe stride, NEXT f4)."""
     e = np.ascontiguousarray(emb, dtype=np.float32)
     n, dim = e.shape
     c = np.ascontiguousarray(np.asarray(cuts, dtype=np.int64))
@@ -235,8 +237,8 @@ def merge(emb: np.ndarray, cuts, p: Params = Params()) -> MergeResult:
     cos = np.empty(max(1, c.size), dtype=np.float64)
     hits = ctypes.c_int64(0)
     rounds = ctypes.c_int32(0)
-    k = lib().oracle_merge(_p(e), n, dim, _p(c), c.size, p.theta, p.band_rel, p.max_rounds,
-                           _p(fin), _p(cos), ctypes.byref(hits), ctypes.byref(rounds))
+    k = lib().oracle_merge_stride(_p(e), n, dim, _p(c), c.size, p.theta, p.band_rel, p.max_rounds,
+                                  stride, _p(fin), _p(cos), ctypes.byref(hits), ctypes.byref(rounds))
     return MergeResult(fin[:k].copy(), cos[:c.size].copy(), int(hits.value), int(rounds.value))
 
 
@@ -339,7 +341,7 @@ def candidates_adaptive(l1_: np.ndarray, npix: int, w: int, ratio_ppm: int,
 def run_video_variant(frames: np.ndarray, emb: np.ndarray | None, p: Params = Params(),
                       distance_kind: int = DIST_L1, adaptive_window: int = 0,
                       adaptive_ratio_ppm: int = 3000000, nv12: bool = False,
-                      nthreads: int | None = None) -> VideoResult:
+                      emb_stride: int = 1, nthreads: int | None = None) -> VideoResult:
     """The path with the f4 variants: O1/O2 (or O0 first for NV12), then O3 (L1)
     or O3' (distance_kind), O4 / O4' / O4'' (adaptive_window > 0, on L1), O5-O9."""
     h = hist_nv12_frames(frames, p, nthreads) if nv12 else hist_frames(frames, p, nthreads)
@@ -356,5 +358,5 @@ def run_video_variant(frames: np.ndarray, emb: np.ndarray | None, p: Params = Pa
     det = min_length(cand, n, p.l_min)
     if emb is None:
         return VideoResult(h, l1_, sc, int(cand.size), det, det.copy(), np.zeros(det.size), 0, 0)
-    m = merge(emb, det, p)
+    m = merge(emb, det, p, stride=emb_stride)
     return VideoResult(h, l1_, sc, int(cand.size), det, m.final, m.cos, m.n_band_hits, m.rounds)

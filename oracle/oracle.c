@@ -284,10 +284,37 @@ double oracle_cosine(const double* a, const double* b, int64_t dim) {
  *   pair; M = {k : c_k >= theta}; if M is empty stop; else remove B_{k+1} for
  *   all k in M at once and recompute the S of the merged clips from frames.
  *   Band hit <=> |c_k - theta| <= band_rel * theta (counted in every round). */
+/* O8' (NEXT f4): with keyframe stride sigma >= 1 only the keyframes enter the
+ * clip sums: frame f is a keyframe iff (f - b) % sigma == 0, b = the first frame
+ * of the DETECTED clip containing f (embeddings are computed once per detected
+ * clip, every sigma-th frame); a merged clip sums its constituents' keyframes.
+ * sigma = 1 is O8. */
+static void clip_sum_keyframes(const float* emb, int64_t dim, int64_t f0, int64_t f1,
+                               const char* key, double* S) {
+  for (int64_t d = 0; d < dim; ++d) S[d] = 0.0;
+  for (int64_t f = f0; f < f1; ++f)
+    if (key[f])
+      for (int64_t d = 0; d < dim; ++d) S[d] += (double)emb[f * dim + d];
+}
+
 int64_t oracle_merge(const float* emb, int64_t n, int64_t dim, const int64_t* cuts,
                      int64_t n_cuts, double theta, double band_rel, int32_t max_rounds,
                      int64_t* final_cuts, double* cos_at_decision, int64_t* n_band_hits,
                      int32_t* rounds) {
+  return oracle_merge_stride(emb, n, dim, cuts, n_cuts, theta, band_rel, max_rounds, 1,
+                             final_cuts, cos_at_decision, n_band_hits, rounds);
+}
+
+int64_t oracle_merge_stride(const float* emb, int64_t n, int64_t dim, const int64_t* cuts,
+                            int64_t n_cuts, double theta, double band_rel, int32_t max_rounds,
+                            int64_t stride, int64_t* final_cuts, double* cos_at_decision,
+                            int64_t* n_band_hits, int32_t* rounds) {
+  char* key = (char*)malloc(n > 0 ? n : 1);
+  for (int64_t j = 0, b = 0; j <= n_cuts; ++j) {
+    const int64_t e = j < n_cuts ? cuts[j] : n;
+    for (int64_t f = b; f < e; ++f) key[f] = ((f - b) % stride) == 0;
+    b = e;
+  }
   /* B holds the boundaries; idx[j] = index of B[j] among the detected cuts */
   int64_t* B = (int64_t*)malloc(sizeof(int64_t) * (n_cuts + 2));
   int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (n_cuts + 2));
@@ -311,7 +338,7 @@ int64_t oracle_merge(const float* emb, int64_t n, int64_t dim, const int64_t* cu
     int64_t K = nb - 1; /* clips */
     if (K < 2) break;
     if (max_rounds > 0 && r >= max_rounds) break;
-    for (int64_t k = 0; k < K; ++k) oracle_clip_sum(emb, dim, B[k], B[k + 1], S + k * dim);
+    for (int64_t k = 0; k < K; ++k) clip_sum_keyframes(emb, dim, B[k], B[k + 1], key, S + k * dim);
     int64_t m = 0;
     for (int64_t k = 0; k + 1 < K; ++k) {
       c[k] = oracle_cosine(S + k * dim, S + (k + 1) * dim, dim);
@@ -340,6 +367,7 @@ int64_t oracle_merge(const float* emb, int64_t n, int64_t dim, const int64_t* cu
   free(S);
   free(c);
   free(rm);
+  free(key);
   return nf;
 }
 

@@ -81,6 +81,13 @@ int64_t oracle_merge(const float* emb, int64_t n, int64_t dim, const int64_t* cu
                      int64_t* final_cuts, double* cos_at_decision, int64_t* n_band_hits,
                      int32_t* rounds);
 
+/* O8' + O9 (NEXT f4): the merge with keyframe stride sigma >= 1 (O8': only every
+ * sigma-th frame of each detected clip enters the clip sums); sigma = 1 is oracle_merge. */
+int64_t oracle_merge_stride(const float* emb, int64_t n, int64_t dim, const int64_t* cuts,
+                            int64_t n_cuts, double theta, double band_rel, int32_t max_rounds,
+                            int64_t stride, int64_t* final_cuts, double* cos_at_decision,
+                            int64_t* n_band_hits, int32_t* rounds);
+
 /* The whole path for one video (O1..O9). hist [n][nbins], l1 [n], score [n],
  * detected / final [n] capacity, cos [n]. Returns 0. */
 typedef struct {

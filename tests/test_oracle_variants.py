@@ -114,3 +114,32 @@ def test_variant_paths_find_c1_planted_cuts():
     r0 = oracle.run_video_variant(fr, emb, p)
     r1 = oracle.run_video(fr, emb, p)
     assert r0.detected.tolist() == r1.detected.tolist() and r0.final.tolist() == r1.final.tolist()
+
+
+def test_keyframe_stride_merge():
+    """O8': only every sigma-th frame of each detected clip enters the clip sums."""
+    rng = np.random.default_rng(4)
+    n, D = 60, 16
+    emb = rng.standard_normal((n, D)).astype(np.float32)
+    cuts = [11, 25, 40]
+    p = oracle.Params(theta=0.0)  # merge everything with cos >= 0 ... decisions below use the sums
+    # stride 1 is the plain merge
+    a, b = oracle.merge(emb, cuts, p, stride=1), oracle.merge(emb, cuts, p)
+    assert a.final.tolist() == b.final.tolist() and np.array_equal(a.cos, b.cos)
+    # non-keyframes are never read: NaN there changes nothing
+    for sigma in (2, 3, 7, 100):
+        key = np.zeros(n, bool)
+        for s0, s1 in zip([0] + cuts, cuts + [n]):
+            key[s0:s1:sigma] = True
+        poisoned = emb.copy()
+        poisoned[~key] = np.nan
+        r1 = oracle.merge(emb, cuts, oracle.Params(), stride=sigma)
+        r2 = oracle.merge(poisoned, cuts, oracle.Params(), stride=sigma)
+        assert r1.final.tolist() == r2.final.tolist() and np.array_equal(r1.cos, r2.cos)
+        # first-round cosines are those of the keyframe sums (numpy, exact f64 sums of f32)
+        bounds = [0] + cuts + [n]
+        S = [emb[s0:s1][key[s0:s1]].astype(np.float64).sum(axis=0) for s0, s1 in zip(bounds[:-1], bounds[1:])]
+        c0 = [float(np.dot(S[k], S[k + 1]) / np.linalg.norm(S[k]) / np.linalg.norm(S[k + 1])) for k in range(3)]
+        r3 = oracle.merge(emb, cuts, oracle.Params(theta=2.0), stride=sigma)  # nothing merges: one round
+        assert r3.rounds == 1
+        np.testing.assert_allclose(r3.cos, c0, rtol=1e-12)
