@@ -81,6 +81,10 @@ typedef struct {
                                  +-w frames of the same video, frames >= 1) and the fixed
                                  rule holds; needs distance = CLIP_DIST_L1                 */
   uint64_t adaptive_ratio_ppm;/* O4'': ratio in ppm (3.0 = 3000000), <= 1e9              */
+  uint32_t emb_stride;        /* O8': keyframe stride sigma (0 or 1 = every frame): only
+                                 frames f with (f - start of their detected clip) % sigma == 0
+                                 enter the clip sums; other embeddings are never read    */
+  uint32_t reserved2;         /* must be 0                                            */
 } clip_params;
 
 #define CLIP_DIST_L1 0u            /* O3: L1 = 2N * total variation (exact integers) */
@@ -124,6 +128,13 @@ int clip_frame_scores(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, in
 int clip_frame_scores_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
                            int32_t width, const uint32_t* prev_hist, uint32_t* hist, uint32_t* l1,
                            float* score);
+
+/* Row a4 alone, from histograms already computed (e.g. the seam frame of a
+ * frame-sharded video, whose predecessor's histogram lives on another GPU).
+ *   hist      device u32 [n_frames][nbins]; prev_hist device u32 [nbins] or NULL
+ *   l1, score as clip_frame_scores (either may be NULL).  Async. */
+int clip_hist_scores(clip_ctx* ctx, const uint32_t* hist, int64_t n_frames, int64_t pixels_per_frame,
+                     const uint32_t* prev_hist, uint32_t* l1, float* score);
 
 /* Streaming cut state of one video; lives in DEVICE memory, zeroed by the
  * caller at video start and passed unchanged between chunks. */

@@ -36,7 +36,8 @@ class ClipParams(ctypes.Structure):
                 ("max_merge_rounds", ctypes.c_uint32), ("merge_cos_threshold", ctypes.c_double),
                 ("band_rel", ctypes.c_double), ("flags", ctypes.c_uint32),
                 ("reserved", ctypes.c_uint32), ("distance", ctypes.c_uint32),
-                ("adaptive_window", ctypes.c_uint32), ("adaptive_ratio_ppm", ctypes.c_uint64)]
+                ("adaptive_window", ctypes.c_uint32), ("adaptive_ratio_ppm", ctypes.c_uint64),
+                ("emb_stride", ctypes.c_uint32), ("reserved2", ctypes.c_uint32)]
 
 
 class ClipVideo(ctypes.Structure):
@@ -72,7 +73,8 @@ FILL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes
 EXPORTS = ["clip_params_default", "clip_detect_init", "clip_detect_destroy", "clip_last_error",
            "clip_frame_scores", "clip_cuts", "clip_merge", "clip_run_videos", "clip_get_stats",
            "clip_debug_binmap", "clip_debug_read_roofline", "clip_frame_scores_nv12",
-           "clip_debug_nv12map", "clip_debug_read_roofline_nv12", "clip_sample_frames"]
+           "clip_debug_nv12map", "clip_debug_read_roofline_nv12", "clip_sample_frames",
+           "clip_hist_scores"]
 
 FORMAT_RGB24 = 0
 FORMAT_NV12 = 1
@@ -111,6 +113,7 @@ def load(build_if_missing: bool = False):
     L.clip_debug_read_roofline.argtypes = [vp, vp, i64, i32, i32]
     L.clip_frame_scores_nv12.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp]
     L.clip_debug_nv12map.argtypes = [vp, vp]
+    L.clip_hist_scores.argtypes = [vp, vp, i64, i64, vp, vp, vp]
     L.clip_sample_frames.argtypes = [vp, vp, i64, i32, i32, vp, i64, i32, i32, i32, vp, vp]
     L.clip_debug_read_roofline_nv12.argtypes = [vp, vp, i64, i32, i32]
     for name in EXPORTS:
@@ -226,6 +229,16 @@ class Ctx:
         self._check(self._lib.clip_frame_scores_nv12(self._h, _ptr(frames), n, H, W, _ptr(prev_hist),
                                                      _ptr(hist), _ptr(l1), _ptr(score)))
         return hist, l1, score
+
+    def hist_scores(self, hist, pixels_per_frame: int, prev_hist=None, l1=None, score=None):
+        """clip_hist_scores: row a4 from existing histograms (device u32/i32 [n, nbins])."""
+        import torch
+        n = hist.shape[0]
+        if l1 is None:
+            l1 = torch.empty(n, dtype=torch.int32, device=hist.device)
+        self._check(self._lib.clip_hist_scores(self._h, _ptr(hist), n, pixels_per_frame,
+                                               _ptr(prev_hist), _ptr(l1), _ptr(score)))
+        return l1, score
 
     def sample_frames(self, frames, cuts, k: int, out_h: int = 224, out_w: int = 224, out=None,
                       want_index: bool = True):

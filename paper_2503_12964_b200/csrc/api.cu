@@ -271,6 +271,7 @@ int validate_params(clip_ctx* ctx, const clip_params* p) {
   if (p->adaptive_window > 0 && p->distance != CLIP_DIST_L1)
     return fail(ctx, CLIP_E_INVALID, "the adaptive threshold is defined on L1 (distance must be L1)");
   if (p->adaptive_ratio_ppm > 1000000000ull) return fail(ctx, CLIP_E_INVALID, "adaptive_ratio_ppm > 1e9");
+  if (p->reserved2 != 0) return fail(ctx, CLIP_E_INVALID, "reserved2 must be 0");
   return CLIP_OK;
 }
 
@@ -353,7 +354,8 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
 
   Span sp(ctx, 2);
   CK(k3_prepare_launch(d_mv, nv, (int32_t)K, d_cuts, s, ctx->stream));
-  CK(k3_piece_sum_launch(d_mv, nv, (int32_t)K, dim, pieces, s, ctx->stream));
+  CK(k3_piece_sum_launch(d_mv, nv, (int32_t)K, dim, pieces,
+                         ctx->p.emb_stride > 1 ? (int32_t)ctx->p.emb_stride : 1, s, ctx->stream));
   CK(k3_clip_sum_launch((int32_t)K, dim, s, ctx->stream));
   ctx->stats.launches += 4;
   int64_t n_alive = K - nv;
@@ -425,6 +427,7 @@ void clip_params_default(clip_params* p) {
   p->distance = CLIP_DIST_L1;
   p->adaptive_window = 0;
   p->adaptive_ratio_ppm = 3000000;
+  p->emb_stride = 1;
 }
 
 int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uintptr_t cuda_stream) {
@@ -549,6 +552,32 @@ int clip_frame_scores_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frame
                            float* score) {
   return frame_scores(ctx, CLIP_FORMAT_NV12, frames, n_frames, height, width, prev_hist, hist,
                       l1, score);
+}
+
+int clip_hist_scores(clip_ctx* ctx, const uint32_t* hist, int64_t n_frames, int64_t pixels_per_frame,
+                     const uint32_t* prev_hist, uint32_t* l1, float* score) {
+  CKS(check_ctx(ctx));
+  if (!hist || n_frames < 1 || pixels_per_frame < 1)
+    return fail(ctx, CLIP_E_INVALID, "bad histograms (n %lld, N %lld)", (long long)n_frames,
+                (long long)pixels_per_frame);
+  const uint32_t nbins = nbins_of(ctx->p);
+  VideoDesc vd{0, n_frames, pixels_per_frame};
+  CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
+  CK(cudaMemcpyAsync(ctx->vids.p, &vd, sizeof vd, cudaMemcpyHostToDevice, ctx->stream));
+  Span sp(ctx, 1);
+  const bool var = ctx->p.distance != CLIP_DIST_L1;
+  CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1,
+                  var ? nullptr : score, ctx->p.cut_threshold_ppm, nullptr, nullptr, ctx->stream));
+  ctx->stats.launches += 1;
+  if (var && score) {
+    int nl = 0;
+    CK(k2_variant_launch(hist, l1, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist,
+                         (int)ctx->p.distance, 0, 0, ctx->p.cut_threshold_ppm, score, nullptr,
+                         nullptr, nullptr, &nl, ctx->stream));
+    ctx->stats.launches += nl;
+  }
+  sp.end();
+  return CLIP_OK;
 }
 
 int clip_cuts(clip_ctx* ctx, const uint32_t* l1, int64_t n_frames, int64_t pixels_per_frame,

@@ -103,8 +103,10 @@ struct MergeScratch {
 
 cudaError_t k3_prepare_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, const int32_t* cuts,
                               MergeScratch s, cudaStream_t stream);
+// stride: O8' keyframe stride (1 = every frame)
 cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim,
-                                int64_t pieces_bound, MergeScratch s, cudaStream_t stream);
+                                int64_t pieces_bound, int32_t stride, MergeScratch s,
+                                cudaStream_t stream);
 cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStream_t stream);
 // one merge round: cosines of the alive boundaries, decisions, ordered
 // compaction alive -> alive2 (the caller swaps the two pointers afterwards).

@@ -127,13 +127,18 @@ __device__ __forceinline__ int32_t find_piece_clip(const int32_t* __restrict__ p
 // P[p][d] = sum of frames of piece p (f64, ascending frames); float4 loads
 // when the rows allow it (D = 768: 192 threads x 4 dims)
 __global__ void __launch_bounds__(kT)
-k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, MergeScratch s) {
+k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, int32_t stride,
+                    MergeScratch s) {
   const int64_t p = blockIdx.x;
   if (p >= s.piece_base[K]) return;
   const int32_t k = find_piece_clip(s.piece_base, K, p);
   const int32_t i = (int32_t)(p - s.piece_base[k]);
-  const int32_t f0 = s.clip_f0[k] + i * kPieceFrames;
-  const int32_t f1 = min(s.clip_f1[k], f0 + kPieceFrames);
+  const int32_t c0 = s.clip_f0[k];
+  // O8' keyframes: (f - c0) % stride == 0 (every frame for stride 1); the
+  // embeddings of other frames are never read
+  const int32_t fp = c0 + i * kPieceFrames;
+  const int32_t f0 = fp + (stride - (fp - c0) % stride) % stride;
+  const int32_t f1 = min(s.clip_f1[k], fp + kPieceFrames);
   const float* __restrict__ e = mv[s.clip_video[k]].emb;
   double* __restrict__ out = s.P + p * dim;
   if ((dim & 3) == 0 && (reinterpret_cast<uintptr_t>(e) & 15) == 0) {
@@ -142,9 +147,9 @@ k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, M
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       const float4* src = reinterpret_cast<const float4*>(e + (int64_t)f0 * dim) + d4;
 #pragma unroll 4
-      for (int32_t f = f0; f < f1; ++f) {
+      for (int32_t f = f0; f < f1; f += stride) {
         const float4 x = __ldg(src);
-        src += d4n;
+        src += (int64_t)d4n * stride;
         a0 += (double)x.x;
         a1 += (double)x.y;
         a2 += (double)x.z;
@@ -158,7 +163,7 @@ k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, M
   }
   for (int32_t d = threadIdx.x; d < dim; d += kT) {
     double acc = 0.0;
-    for (int32_t f = f0; f < f1; ++f) acc += (double)__ldg(e + (int64_t)f * dim + d);
+    for (int32_t f = f0; f < f1; f += stride) acc += (double)__ldg(e + (int64_t)f * dim + d);
     out[d] = acc;
   }
 }
@@ -305,10 +310,11 @@ cudaError_t k3_prepare_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, con
 }
 
 cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim,
-                                int64_t pieces_bound, MergeScratch s, cudaStream_t stream) {
+                                int64_t pieces_bound, int32_t stride, MergeScratch s,
+                                cudaStream_t stream) {
   (void)nv;
   if (K <= 0 || pieces_bound <= 0) return cudaSuccess;
-  k3_piece_sum_kernel<<<(unsigned)pieces_bound, kT, 0, stream>>>(d_mv, K, dim, s);
+  k3_piece_sum_kernel<<<(unsigned)pieces_bound, kT, 0, stream>>>(d_mv, K, dim, stride, s);
   return cudaGetLastError();
 }
 

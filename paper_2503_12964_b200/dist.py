@@ -118,19 +118,26 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     rank = dist.get_rank(group)
     m, H, W, _ = frames.shape
     dev = frames.device
+    shards = frame_shards(n_total, world)
+    width = max(b - a for a, b in shards)
+    # (4, issued first) the embeddings do not depend on the scan: their
+    # all-gather runs on NCCL's stream while K1 scans the shard
+    e_work = None
+    if emb_all is None:
+        D = emb.shape[1]
+        epad = torch.zeros((width, D), dtype=emb.dtype, device=dev)
+        epad[:m].copy_(emb)
+        e_all = torch.empty(world * width * D, dtype=emb.dtype, device=dev)
+        e_work = dist.all_gather_into_tensor(e_all, epad.view(-1), group=group, async_op=True)
     hist, l1, _ = ctx.frame_scores(frames, want_score=False)
     nb = hist.shape[1]
-    # (2) last histograms of every shard
+    # (2) last histograms of every shard; the seam frame's L1 from histograms (K2 only)
     lasts = torch.empty(world * nb, dtype=hist.dtype, device=dev)
     dist.all_gather_into_tensor(lasts, hist[m - 1].contiguous(), group=group)
     lasts = lasts.view(world, nb)
     if rank > 0:
-        _, l1_first, _ = ctx.frame_scores(frames[:1], prev_hist=lasts[rank - 1].contiguous(),
-                                          want_score=False)
-        l1[:1].copy_(l1_first)
+        ctx.hist_scores(hist[:1], H * W, prev_hist=lasts[rank - 1].contiguous(), l1=l1[:1])
     # (3) whole-video L1 on every rank; shards are padded to a common length
-    shards = frame_shards(n_total, world)
-    width = max(b - a for a, b in shards)
     pad = torch.zeros(width, dtype=l1.dtype, device=dev)
     pad[:m].copy_(l1)
     l1_all = torch.empty(world * width, dtype=l1.dtype, device=dev)
@@ -142,11 +149,7 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     n_cuts = int(state[3].item())
     # (4) embeddings of the whole video, then the merge
     if emb_all is None:
-        D = emb.shape[1]
-        epad = torch.zeros((width, D), dtype=emb.dtype, device=dev)
-        epad[:m].copy_(emb)
-        e_all = torch.empty(world * width * D, dtype=emb.dtype, device=dev)
-        dist.all_gather_into_tensor(e_all, epad.view(-1), group=group)
+        e_work.wait()
         e_all = e_all.view(world * width, D)
         emb_all = torch.cat([e_all[r * width:r * width + (b - a)] for r, (a, b) in enumerate(shards)])
     merged, cos, hits, rounds = ctx.merge(emb_all, cuts[:max(1, n_cuts)].contiguous(), n_cuts=n_cuts)

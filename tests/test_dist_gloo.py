@@ -119,6 +119,18 @@ class _OracleCtx:
             l1, _ = oracle.l1(h, npix)
         return (torch.from_numpy(h.view(np.int32).copy()), torch.from_numpy(l1.view(np.int32).copy()), None)
 
+    def hist_scores(self, hist, npix, prev_hist=None, l1=None):
+        import oracle
+        import torch
+        h = hist.numpy().view(np.uint32)
+        if prev_hist is not None:
+            h = np.concatenate([prev_hist.numpy().view(np.uint32)[None], h])
+        v, _ = oracle.l1(h, npix)
+        if prev_hist is not None:
+            v = v[1:]
+        l1.copy_(torch.from_numpy(v.view(np.int32).copy()))
+        return l1, None
+
     def cuts(self, l1, npix, state, cuts, is_final):
         import oracle
         a = l1.numpy().view(np.uint32)

@@ -84,6 +84,33 @@ def test_sample_after_run_videos_c2_prefix(ctx, dev):
         assert np.array_equal(got[j], oracle.resize_linear(fr, 224, 224)), (j, t)
 
 
+def test_sample_full_c2_in_bench_configuration(ctx, dev):
+    """The whole C2 video (18,000 x 720p, resident) -> clip_run_videos -> final
+    cuts -> K4 with k = 8 at 224x224, exactly as bench.py's f3_sample times it;
+    every sampled index checked, every 13th output frame against the oracle."""
+    v = manifest.c2_video()
+    table = torch_dev.frame_table(v, dev)
+    frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+    torch_dev.gen_frames(v, table, frames)
+    emb = torch.empty((v.n, manifest.EMB_DIM), dtype=torch.float32, device=dev)
+    torch_dev.gen_emb(v, table, emb)
+    res = ctx.run_videos([{"n": v.n, "H": v.H, "W": v.W, "frames": frames, "emb": emb}])[0]
+    cuts = torch.from_numpy(res.final.astype(np.int32)).to(dev)
+    out, idx = ctx.sample_frames(frames, cuts, 8, 224, 224)
+    idx_h = idx.cpu().numpy()
+    bounds = [0] + res.final.tolist() + [v.n]
+    want = [oracle.sample_index(bounds[c], bounds[c + 1], i, 8) for c in range(len(bounds) - 1)
+            for i in range(8)]
+    assert idx_h.tolist() == want
+    got = out.cpu().numpy()
+    for j in range(0, idx_h.size, 13):
+        t = int(idx_h[j])
+        fr = synth.gen_frames(v, t0=t, n=1)[0]
+        assert np.array_equal(got[j], oracle.resize_linear(fr, 224, 224)), (j, t)
+    del frames, out
+    torch.cuda.empty_cache()
+
+
 def test_sample_invalid(ctx, dev):
     from paper_2503_12964_b200 import ClipError
     fr = torch.zeros((4, 16, 16, 3), dtype=torch.uint8, device=dev)

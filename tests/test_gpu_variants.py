@@ -112,3 +112,27 @@ def test_streaming_cuts_reject_variants(dev):
     c.close()
     with pytest.raises(ClipError):  # adaptive needs the L1 distance
         _ctx(distance=1, adaptive_window=2)
+
+
+@pytest.mark.parametrize("sigma", [2, 5, 16, 40])
+def test_keyframe_stride_matches_oracle(dev, sigma):
+    """O8': only every sigma-th frame of each detected clip is summed; the
+    other embeddings are NaN here and must never be read."""
+    items, hosts = _videos(dev)
+    c = _ctx(emb_stride=sigma)
+    ref0 = [oracle.run_video(h, e) for h, e in hosts]  # detected cuts (stride-independent)
+    for it, (host, emb), r0 in zip(items, hosts, ref0):
+        key = np.zeros(host.shape[0], bool)
+        b = [0] + r0.detected.tolist() + [host.shape[0]]
+        for s0, s1 in zip(b[:-1], b[1:]):
+            key[s0:s1:sigma] = True
+        poisoned = emb.copy()
+        poisoned[~key] = np.nan
+        it["emb"] = torch.from_numpy(poisoned).to(dev)
+    res = c.run_videos(items, want_cos=True)
+    c.close()
+    for r, (host, emb) in zip(res, hosts):
+        ref = oracle.run_video_variant(host, emb, oracle.Params(), emb_stride=sigma)
+        assert list(r.detected) == list(ref.detected) and list(r.final) == list(ref.final)
+        np.testing.assert_allclose(r.detected_cos, ref.cos, rtol=COS_RTOL, atol=1e-12)
+        assert r.rounds == ref.rounds
