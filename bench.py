@@ -619,6 +619,12 @@ def run_shard_frames(args):
         e1.record(stream)
         torch.cuda.synchronize()
     st = ctx.stats(reset=True)
+    # one extra (untimed) step with CUDA events between the phases of the exchange
+    marks = []
+    with torch.cuda.stream(stream):
+        cdist.run_video_sharded(ctx, frames, emb, v.n, a, marks=marks)
+    torch.cuda.synchronize()
+    phase_ms = [round(marks[i].elapsed_time(marks[i + 1]), 4) for i in range(len(marks) - 1)]
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
     allt = torch.empty(world, dtype=torch.float64, device=dev)
     dist.all_gather_into_tensor(allt, t)
@@ -642,6 +648,9 @@ def run_shard_frames(args):
             "hbm_gbs": round(v.n * v.frame_bytes / (ms * 1e-3) / 1e9, 1),
             "per_rank_ms_per_step": [round(x, 4) for x in per_rank],
             "k1_ms_per_step_rank0": round(st["k1_ms"] / args.steps, 4),
+            "phase_ms_rank0": dict(zip(["scan (K1+L1)", "seam (all-gather lasts, a4)",
+                                        "L1 all-gather + cuts", "embeddings wait + concat",
+                                        "merge"], phase_ms)),
             "gpu_launches": int(st["launches"]), "clocks": clk.summary(), "parity_vs_golden": parity,
         }
         print(json.dumps(line), flush=True)

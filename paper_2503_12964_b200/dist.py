@@ -96,7 +96,8 @@ def frame_shards(n: int, world: int) -> list:
     return [(n * r // world, n * (r + 1) // world) for r in range(world)]
 
 
-def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_all=None):
+def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_all=None,
+                      marks=None):
     """One long video split by frame ranges across the ranks of `group`
     (the context-parallel analogue on the frame axis).
 
@@ -111,6 +112,8 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
       4. all_gather of the embeddings -> clip_merge on the whole video.
     Results are identical to the single-GPU path (same kernels, same order).
     `frames`: u8 cuda [m, H, W, 3] = frames f0..f0+m-1; `emb`: f32 cuda [m, D].
+    `marks`: optional list; CUDA events recorded after each phase are appended
+    (diagnosis of the exchange overhead).
     Returns (detected list, final list, cos tensor, band hits, rounds)."""
     import torch
     import torch.distributed as dist
@@ -129,7 +132,15 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
         epad[:m].copy_(emb)
         e_all = torch.empty(world * width * D, dtype=emb.dtype, device=dev)
         e_work = dist.all_gather_into_tensor(e_all, epad.view(-1), group=group, async_op=True)
+    def mark():
+        if marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(dev))
+            marks.append(ev)
+
+    mark()
     hist, l1, _ = ctx.frame_scores(frames, want_score=False)
+    mark()
     nb = hist.shape[1]
     # (2) last histograms of every shard; the seam frame's L1 from histograms (K2 only)
     lasts = torch.empty(world * nb, dtype=hist.dtype, device=dev)
@@ -137,6 +148,7 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     lasts = lasts.view(world, nb)
     if rank > 0:
         ctx.hist_scores(hist[:1], H * W, prev_hist=lasts[rank - 1].contiguous(), l1=l1[:1])
+    mark()
     # (3) whole-video L1 on every rank; shards are padded to a common length
     pad = torch.zeros(width, dtype=l1.dtype, device=dev)
     pad[:m].copy_(l1)
@@ -147,10 +159,13 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     cuts = torch.empty(n_total // ctx.params.min_clip_frames + 2, dtype=torch.int32, device=dev)
     ctx.cuts(l1_full, H * W, state, cuts, True)
     n_cuts = int(state[3].item())
+    mark()
     # (4) embeddings of the whole video, then the merge
     if emb_all is None:
         e_work.wait()
         e_all = e_all.view(world * width, D)
         emb_all = torch.cat([e_all[r * width:r * width + (b - a)] for r, (a, b) in enumerate(shards)])
+    mark()
     merged, cos, hits, rounds = ctx.merge(emb_all, cuts[:max(1, n_cuts)].contiguous(), n_cuts=n_cuts)
+    mark()
     return (cuts[:n_cuts].cpu().tolist(), merged.cpu().tolist(), cos, hits, rounds)
