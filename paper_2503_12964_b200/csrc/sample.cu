@@ -18,6 +18,7 @@
 // and store them (the output is ~8 % of the bytes read).  Many CTAs per SM
 // keep the copies of several bands in flight.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -27,7 +28,7 @@ namespace clipdetect {
 namespace {
 
 constexpr int kK4Threads = 256;
-constexpr int kK4SmemRows = 40 * 1024;  // budget for the staged source rows per CTA
+constexpr int kK4SmemRows = 24 * 1024;  // staged source rows per CTA (swept: tools/k4_micro.py)
 constexpr int kK4MaxW2 = 4096;
 
 struct LinCoeff {
@@ -127,7 +128,12 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
 
 int k4_rows_per_band(int32_t W) {
   const int32_t slot = ((3 * W + 32) + 15) & ~15;
-  int32_t rb = kK4SmemRows / (2 * slot);
+  int32_t budget = kK4SmemRows;
+  if (const char* e = getenv("CLIPDETECT_K4_BUDGET_KB")) {  // tuning hook (tools/k4_micro.py)
+    const int kb = atoi(e);
+    if (kb >= 4 && kb <= 200) budget = kb * 1024;
+  }
+  int32_t rb = budget / (2 * slot);
   if (rb > 32) rb = 32;
   return rb < 1 ? 1 : rb;
 }
