@@ -194,14 +194,23 @@ CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
   const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
   return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
 }
-CD_HD uint32_t lut_index(uint32_t na, uint32_t d, bool swz = true) {
-  return d * 256u + (swz ? (na ^ d) : na);
+// Bank swizzles of the table (the bank of entry (d, na) is bits 2-6 of the
+// byte index): 0 none; 1 na ^ d; 2 na ^ ((d << 2) & 0xFC), i.e. bank =
+// (d ^ (na >> 2)) & 31 — rows d and d+1 land in different banks, which keeps
+// the lookups of a warp on smooth content (d, na jittering by +-1 around a few
+// values, e.g. decoded NV12 where the luma noise moves r, g, b together)
+// nearly conflict-free (bank-conflict simulation in DESIGN.md §7).
+CD_HD uint32_t lut_swizzle(uint32_t d, int swz) {
+  return swz == 2 ? ((d << 2) & 0xFCu) : (swz == 1 ? d : 0u);
+}
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d, int swz = 1) {
+  return d * 256u + (na ^ lut_swizzle(d, swz));
 }
 
 // Part 1 (before the table lookups): returns the partial code and the two
 // lanes' table indices.  The sector is carried as the three raw ordering
 // flags A, B, C (parity is decoded from them in code_to_bin_lut).
-template <bool SWZ = true>
+template <int SWZ = 1>
 CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   constexpr uint32_t kB15 = 0x80008000u;
@@ -210,7 +219,8 @@ CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t d = cd_mad(mn, k.neg1, mx);
   const uint32_t sum = cd_mad(B, k.one, cd_mad(R, k.one, G));
   const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, sum));  // mid - min
-  const uint32_t nas = SWZ ? (na ^ d) : na;                          // bank swizzle
+  // bank swizzle (lut_swizzle, both lanes at once)
+  const uint32_t nas = SWZ == 2 ? (na ^ (cd_mad(d, 4u, 0u) & 0x00FC00FCu)) : (SWZ == 1 ? (na ^ d) : na);
   i0 = cd_prmt(nas, d, 0x1140u);  // lane 0: nas | d << 8
   i1 = cd_prmt(nas, d, 0x3362u);  // lane 1
   const uint32_t R15 = cd_mad(R, k.one, kB15);

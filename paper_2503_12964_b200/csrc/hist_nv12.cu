@@ -40,6 +40,7 @@ constexpr int kNvStageBytes = 24576;  // 3 * R * W <= 24576  <=>  R * W <= 8192
 constexpr int kNvWarps = 16;
 constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvLutBytes = 65536;
+constexpr int kNvSwz = 2;  // table swizzle (binfn.cuh lut_swizzle): conflict-free rows on NV12 content
 
 struct NvSmem {
   alignas(128) uint8_t buf[kNvStages][kNvStageBytes];
@@ -125,7 +126,7 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, c
       uint32_t R, G, B;
       nv12_pair_rgb(__byte_perm(w, 0u, 0x4440u | o), __byte_perm(w, 0u, 0x4440u | (o + 1)), ruv,
                     guv, buv, R, G, B);
-      pre[2 * k + r] = code_pair_lut_pre<true>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
+      pre[2 * k + r] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
     }
   }
   uint32_t qa[8], qb[8];
@@ -162,7 +163,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     }
     for (int i = tid; i < 256; i += blockDim.x) sm.binacc[i] = 0u;
     for (int i = tid; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ d;
+      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, kNvSwz);
       sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
   }
@@ -348,7 +349,7 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
   extern __shared__ __align__(16) uint8_t lut[];
   if (FAST) {
     for (int i = threadIdx.x; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ d;
+      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, kNvSwz);
       lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
     __syncthreads();
@@ -363,7 +364,7 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
     uint32_t b0, b1;
     if (FAST) {
       uint32_t i0, i1;
-      const uint32_t pre = code_pair_lut_pre<true>(R, G, B, mk, i0, i1);
+      const uint32_t pre = code_pair_lut_pre<kNvSwz>(R, G, B, mk, i0, i1);
       const uint32_t code = code_pair_lut_post(pre, lut[i0], lut[i1], mk);
       b0 = code_to_bin_lut(lut_off_lo(code, mk) >> 2);
       b1 = code_to_bin_lut(lut_off_hi(code, mk) >> 2);

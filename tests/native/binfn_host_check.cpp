@@ -23,6 +23,9 @@ int main(int argc, char** argv) {
   std::vector<uint8_t> lut(65536, 0);
   for (uint32_t d = 0; d < 256; ++d)
     for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d)] = (uint8_t)lut_entry(na, d);
+  std::vector<uint8_t> lut2(65536, 0);  // swizzle 2 (the NV12 kernel's table)
+  for (uint32_t d = 0; d < 256; ++d)
+    for (uint32_t na = 0; na <= d; ++na) lut2[lut_index(na, d, 2)] = (uint8_t)lut_entry(na, d);
   for (uint32_t c = 0; c < N; ++c) {
     const uint32_t c2 = c ^ 0xA5A5A5u;
     const uint32_t R = (c >> 16) | ((c2 >> 16) << 16);
@@ -73,8 +76,8 @@ int main(int argc, char** argv) {
     uint32_t R, G, B;
     nv12_pair_rgb(Y, Y2, ruv, guv, buv, R, G, B);
     uint32_t i0, i1;
-    const uint32_t pre = code_pair_lut_pre(R, G, B, kMadK, i0, i1);
-    const uint32_t lc = code_pair_lut_post(pre, lut[i0], lut[i1], kMadK);
+    const uint32_t pre = code_pair_lut_pre<2>(R, G, B, kMadK, i0, i1);
+    const uint32_t lc = code_pair_lut_post(pre, lut2[i0], lut2[i1], kMadK);
     n0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
     n1[(Y2 << 16) | (U << 8) | V] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);
   }
