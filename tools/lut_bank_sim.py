@@ -1,11 +1,16 @@
 #!/usr/bin/env python3
 """Shared-memory bank-conflict simulation of the hue-table (LUT) lookups of K1 and
 K1-NV12 for the table swizzles of binfn.cuh (lut_swizzle), on C2 content and noise:
-average wavefronts per warp-wide LDS.U8.  Run: PYTHONPATH=. python tools/lut_bank_sim.py"""
+average wavefronts per warp-wide LDS.U8.  Run: PYTHONPATH=. python tools/lut_bank_sim.py
+(NV12 -> RGB through OpenCV's COLOR_YUV2RGB_NV12, the conversion reading O0 names.)"""
+import cv2
+import numpy as np
+
+import synth
 from synth import manifest
 v = manifest.subsample(manifest.c2_video(0), 40)
 nv = synth.gen_nv12(v)[::8]     # 5 frames
-rgbs = np.stack([oracle.nv12_to_rgb(f) for f in nv]).astype(np.int32)
+rgbs = np.stack([cv2.cvtColor(f, cv2.COLOR_YUV2RGB_NV12) for f in nv]).astype(np.int32)
 rgb_direct = synth.gen_frames(v)[::8].astype(np.int32)
 
 def dn(rgb):
@@ -69,6 +74,6 @@ def nv12_instrs4(rgb, swz, n=4000):
 for swz in ['xor', 'xor4']:
     print('2x4 units', swz, 'NV12-c2', round(wavefronts(nv12_instrs4(rgbs, swz)), 2))
 nz12 = rng.integers(0, 256, (2, H * 3 // 2, W), dtype=np.uint8)
-nzrgb = np.stack([oracle.nv12_to_rgb(f) for f in nz12]).astype(np.int32)
+nzrgb = np.stack([cv2.cvtColor(f, cv2.COLOR_YUV2RGB_NV12) for f in nz12]).astype(np.int32)
 for swz in ['xor', 'xor4']:
     print('NV12-noise', swz, round(wavefronts(nv12_instrs(nzrgb, swz)), 2))
