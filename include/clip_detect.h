@@ -190,6 +190,13 @@ int clip_sample_frames(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, i
                        int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k, int32_t out_h,
                        int32_t out_w, uint8_t* out, int32_t* index);
 
+/* clip_sample_frames for NV12 frames (device u8 [n_frames][height*3/2][width]): each
+ * bilinear tap is converted by O0 before O11 — identical to converting the whole frame
+ * to RGB24 first.  Same outputs, errors and asynchrony as clip_sample_frames. */
+int clip_sample_frames_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                            int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k,
+                            int32_t out_h, int32_t out_w, uint8_t* out, int32_t* index);
+
 /* ---------------------------------------------------------------- batch API */
 
 #define CLIP_FORMAT_RGB24 0 /* u8 [n][H][W][3]                */

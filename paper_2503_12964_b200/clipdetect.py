@@ -74,7 +74,7 @@ EXPORTS = ["clip_params_default", "clip_detect_init", "clip_detect_destroy", "cl
            "clip_frame_scores", "clip_cuts", "clip_merge", "clip_run_videos", "clip_get_stats",
            "clip_debug_binmap", "clip_debug_read_roofline", "clip_frame_scores_nv12",
            "clip_debug_nv12map", "clip_debug_read_roofline_nv12", "clip_sample_frames",
-           "clip_hist_scores"]
+           "clip_hist_scores", "clip_sample_frames_nv12"]
 
 FORMAT_RGB24 = 0
 FORMAT_NV12 = 1
@@ -115,6 +115,7 @@ def load(build_if_missing: bool = False):
     L.clip_debug_nv12map.argtypes = [vp, vp]
     L.clip_hist_scores.argtypes = [vp, vp, i64, i64, vp, vp, vp]
     L.clip_sample_frames.argtypes = [vp, vp, i64, i32, i32, vp, i64, i32, i32, i32, vp, vp]
+    L.clip_sample_frames_nv12.argtypes = [vp, vp, i64, i32, i32, vp, i64, i32, i32, i32, vp, vp]
     L.clip_debug_read_roofline_nv12.argtypes = [vp, vp, i64, i32, i32]
     for name in EXPORTS:
         if name not in ("clip_params_default", "clip_last_error"):
@@ -242,18 +243,25 @@ class Ctx:
 
     def sample_frames(self, frames, cuts, k: int, out_h: int = 224, out_w: int = 224, out=None,
                       want_index: bool = True):
-        """clip_sample_frames (NEXT f3): k frames per clip of one RGB24 video,
-        resized to out_h x out_w.  ``cuts``: device int32 tensor of final cuts.
+        """clip_sample_frames (NEXT f3): k frames per clip of one RGB24 video
+        ([n, H, W, 3]) or NV12 video ([n, H*3/2, W]), resized to out_h x out_w.  ``cuts``: device int32 tensor of final cuts.
         Returns (out u8 [(n_cuts+1)*k, out_h, out_w, 3], index int32 tensor or None)."""
         import torch
-        n, H, W, C = frames.shape
-        assert C == 3 and frames.is_cuda
+        nv12 = frames.dim() == 3  # NV12 surfaces [n, H*3/2, W]
+        if nv12:
+            n, H3, W = frames.shape
+            H = H3 * 2 // 3
+        else:
+            n, H, W, C = frames.shape
+            assert C == 3
+        assert frames.is_cuda
         n_cuts = 0 if cuts is None else cuts.numel()
         m = (n_cuts + 1) * k
         if out is None:
             out = torch.empty((m, out_h, out_w, 3), dtype=torch.uint8, device=frames.device)
         idx = torch.empty(m, dtype=torch.int32, device=frames.device) if want_index else None
-        self._check(self._lib.clip_sample_frames(self._h, _ptr(frames), n, H, W,
+        fn = self._lib.clip_sample_frames_nv12 if nv12 else self._lib.clip_sample_frames
+        self._check(fn(self._h, _ptr(frames), n, H, W,
                                                  _ptr(cuts) if n_cuts else None, n_cuts, k, out_h,
                                                  out_w, _ptr(out), _ptr(idx)))
         return out, idx

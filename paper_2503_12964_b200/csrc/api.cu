@@ -892,11 +892,14 @@ int clip_debug_binmap(clip_ctx* ctx, uint8_t* table) {
   return CLIP_OK;
 }
 
-int clip_sample_frames(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
-                       int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k, int32_t out_h,
-                       int32_t out_w, uint8_t* out, int32_t* index) {
+}  // extern "C"
+
+namespace {
+int sample_frames(clip_ctx* ctx, int format, const uint8_t* frames, int64_t n_frames,
+                  int32_t height, int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k,
+                  int32_t out_h, int32_t out_w, uint8_t* out, int32_t* index) {
   CKS(check_ctx(ctx));
-  CKS(validate_frames(ctx, frames, n_frames, height, width, false));
+  CKS(validate_frames(ctx, frames, n_frames, height, width, false, format));
   if (n_cuts < 0 || n_cuts >= n_frames || (n_cuts > 0 && !cuts))
     return fail(ctx, CLIP_E_INVALID, "bad cuts (n_cuts %lld)", (long long)n_cuts);
   if (k < 1 || out_h < 1 || out_w < 1 || out_w > k4_max_width())
@@ -906,10 +909,27 @@ int clip_sample_frames(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, i
     return fail(ctx, CLIP_E_INVALID, "too many output frames");
   Span sp(ctx, 2);
   CK(k4_sample_launch(frames, n_frames, height, width, cuts, (int32_t)n_cuts, k, out_h, out_w, out,
-                      index, ctx->stream));
+                      index, format == CLIP_FORMAT_NV12, ctx->stream));
   sp.end();
   ctx->stats.launches += 1;
   return CLIP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int clip_sample_frames(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                       int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k, int32_t out_h,
+                       int32_t out_w, uint8_t* out, int32_t* index) {
+  return sample_frames(ctx, CLIP_FORMAT_RGB24, frames, n_frames, height, width, cuts, n_cuts, k,
+                       out_h, out_w, out, index);
+}
+
+int clip_sample_frames_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frames, int32_t height,
+                            int32_t width, const int32_t* cuts, int64_t n_cuts, int32_t k,
+                            int32_t out_h, int32_t out_w, uint8_t* out, int32_t* index) {
+  return sample_frames(ctx, CLIP_FORMAT_NV12, frames, n_frames, height, width, cuts, n_cuts, k,
+                       out_h, out_w, out, index);
 }
 
 int clip_debug_nv12map(clip_ctx* ctx, uint8_t* table) {

@@ -36,11 +36,11 @@ cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t n
                               cudaStream_t stream);
 
 // ---- K4 (sample.cu): clip frame sampling + resize (NEXT f3)
-int k4_rows_per_band(int32_t W);
+int k4_rows_per_band(int32_t W, bool nv12);
 int k4_max_width();
 cudaError_t k4_sample_launch(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
                              const int32_t* cuts, int32_t n_cuts, int32_t k, int32_t H2, int32_t W2,
-                             uint8_t* out, int32_t* index, cudaStream_t stream);
+                             uint8_t* out, int32_t* index, bool nv12, cudaStream_t stream);
 
 // ---- K2 (cuts.cu)
 struct VideoDesc {

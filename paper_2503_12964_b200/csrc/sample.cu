@@ -20,6 +20,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include "binfn.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -59,6 +60,22 @@ __device__ __forceinline__ LinCoeff lin_coeff(int32_t src, int32_t dst, int32_t 
   return c;
 }
 
+// One source pixel of an NV12 frame -> (r, g, b) by reading O0 (scalar).
+__device__ __forceinline__ void nv12_px(const uint8_t* yrow, const uint8_t* uvrow, int32_t x,
+                                        int32_t& r, int32_t& g, int32_t& b) {
+  int32_t ruv, guv, buv;
+  const int32_t xc = x & ~1;
+  nv12_chroma(uvrow[xc], uvrow[xc + 1], ruv, guv, buv);
+  const int32_t l = nv12_luma(yrow[x]);
+  r = min(max((l + ruv) >> 20, 0), 255);
+  g = min(max((l + guv) >> 20, 0), 255);
+  b = min(max((l + buv) >> 20, 0), 255);
+}
+
+// NV12: frames are u8 [n][H*3/2][W]; the band stages, per output row, the two
+// Y rows and the two UV rows (y/2) its taps use, and converts each tap (O0)
+// before the resize (O11) -- identical to converting the whole frame first.
+template <bool NV12>
 __global__ void __launch_bounds__(kK4Threads)
 k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32_t W,
                  const int32_t* __restrict__ cuts, int32_t n_cuts, int32_t k, int32_t H2, int32_t W2,
@@ -80,8 +97,9 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
   if (band == 0 && threadIdx.x == 0 && index) index[j] = (int32_t)t;
 
   const int32_t r0 = band * rb, nr = min(rb, H2 - r0);
-  const int64_t row_bytes = 3 * (int64_t)W;
-  const uint8_t* fb = frames + t * (int64_t)H * row_bytes;
+  constexpr int kRowsPerOut = NV12 ? 4 : 2;
+  const int64_t row_bytes = NV12 ? (int64_t)W : 3 * (int64_t)W;
+  const uint8_t* fb = frames + t * (NV12 ? 3 * (int64_t)H * W / 2 : (int64_t)H * row_bytes);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -89,10 +107,13 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint64_t pol = policy_evict_first();
-    for (int32_t q = 0; q < 2 * nr; ++q) {
-      const LinCoeff yc = lin_coeff(H, H2, r0 + (q >> 1));
-      if ((q & 1) == 0) ycs[q >> 1] = yc;
-      const uint8_t* row = fb + (int64_t)(q & 1 ? yc.s1 : yc.s0) * row_bytes;
+    for (int32_t q = 0; q < kRowsPerOut * nr; ++q) {
+      const int32_t dy = q / kRowsPerOut, which = q % kRowsPerOut;
+      const LinCoeff yc = lin_coeff(H, H2, r0 + dy);
+      if (which == 0) ycs[dy] = yc;
+      const int32_t sy = which & 1 ? yc.s1 : yc.s0;
+      const uint8_t* row = which < 2 ? fb + (int64_t)sy * row_bytes                 // Y or RGB row
+                                     : fb + (int64_t)H * W + (int64_t)(sy >> 1) * W;  // UV row
       const uintptr_t a0 = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;
       const uintptr_t a1 = (reinterpret_cast<uintptr_t>(row) + row_bytes + 15) & ~(uintptr_t)15;
       row_off[q] = (int32_t)(reinterpret_cast<uintptr_t>(row) - a0);
@@ -111,13 +132,31 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
     const int32_t dy = p / W2, dx = p - dy * W2;
     const LinCoeff yc = ycs[dy];
     const LinCoeff x = xc[dx];
-    const uint8_t* q0 = rows + (int64_t)(2 * dy) * slot_bytes + row_off[2 * dy];
-    const uint8_t* q1 = rows + (int64_t)(2 * dy + 1) * slot_bytes + row_off[2 * dy + 1];
-    const int32_t o0 = 3 * x.s0, o1 = 3 * x.s1;
+    const int32_t base = kRowsPerOut * dy;
+    const uint8_t* q0 = rows + (int64_t)base * slot_bytes + row_off[base];
+    const uint8_t* q1 = rows + (int64_t)(base + 1) * slot_bytes + row_off[base + 1];
+    int32_t p00[3], p01[3], p10[3], p11[3];
+    if constexpr (NV12) {
+      const uint8_t* u0 = rows + (int64_t)(base + 2) * slot_bytes + row_off[base + 2];
+      const uint8_t* u1 = rows + (int64_t)(base + 3) * slot_bytes + row_off[base + 3];
+      nv12_px(q0, u0, x.s0, p00[0], p00[1], p00[2]);
+      nv12_px(q0, u0, x.s1, p01[0], p01[1], p01[2]);
+      nv12_px(q1, u1, x.s0, p10[0], p10[1], p10[2]);
+      nv12_px(q1, u1, x.s1, p11[0], p11[1], p11[2]);
+    } else {
+      const int32_t o0 = 3 * x.s0, o1 = 3 * x.s1;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        p00[ch] = q0[o0 + ch];
+        p01[ch] = q0[o1 + ch];
+        p10[ch] = q1[o0 + ch];
+        p11[ch] = q1[o1 + ch];
+      }
+    }
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const int32_t h0 = q0[o0 + ch] * x.w0 + q0[o1 + ch] * x.w1;
-      const int32_t h1 = q1[o0 + ch] * x.w0 + q1[o1 + ch] * x.w1;
+      const int32_t h0 = p00[ch] * x.w0 + p01[ch] * x.w1;
+      const int32_t h1 = p10[ch] * x.w0 + p11[ch] * x.w1;
       const int32_t v = ((((h0 >> 4) * yc.w0) >> 16) + (((h1 >> 4) * yc.w1) >> 16) + 2) >> 2;
       ob[(int64_t)p * 3 + ch] = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
     }
@@ -126,15 +165,15 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
 
 }  // namespace
 
-int k4_rows_per_band(int32_t W) {
-  const int32_t slot = ((3 * W + 32) + 15) & ~15;
+int k4_rows_per_band(int32_t W, bool nv12) {
+  const int32_t slot = (((nv12 ? W : 3 * W) + 32) + 15) & ~15;
   int32_t budget = kK4SmemRows;
   if (const char* e = getenv("CLIPDETECT_K4_BUDGET_KB")) {  // tuning hook (tools/k4_micro.py)
     const int kb = atoi(e);
     if (kb >= 4 && kb <= 200) budget = kb * 1024;
   }
-  int32_t rb = budget / (2 * slot);
-  if (rb > 32) rb = 32;
+  int32_t rb = budget / ((nv12 ? 4 : 2) * slot);
+  if (rb > (nv12 ? 16 : 32)) rb = nv12 ? 16 : 32;
   return rb < 1 ? 1 : rb;
 }
 
@@ -142,20 +181,19 @@ int k4_max_width() { return kK4MaxW2; }
 
 cudaError_t k4_sample_launch(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
                              const int32_t* cuts, int32_t n_cuts, int32_t k, int32_t H2, int32_t W2,
-                             uint8_t* out, int32_t* index, cudaStream_t stream) {
-  const int32_t rb = k4_rows_per_band(W);
-  const int32_t slot = ((3 * W + 32) + 15) & ~15;
+                             uint8_t* out, int32_t* index, bool nv12, cudaStream_t stream) {
+  const int32_t rb = k4_rows_per_band(W, nv12);
+  const int32_t slot = (((nv12 ? W : 3 * W) + 32) + 15) & ~15;
   const int32_t bands = (H2 + rb - 1) / rb;
-  const size_t smem = ((sizeof(LinCoeff) * W2 + 127) & ~(size_t)127) + (size_t)2 * rb * slot;
-  cudaError_t e = cudaFuncSetAttribute(k4_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  const size_t smem = ((sizeof(LinCoeff) * W2 + 127) & ~(size_t)127) + (size_t)(nv12 ? 4 : 2) * rb * slot;
+  auto kern = nv12 ? k4_sample_kernel<true> : k4_sample_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (int64_t)(n_cuts + 1) * k * bands;
   if (blocks <= 0) return cudaSuccess;
   if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
-  k4_sample_kernel<<<(unsigned)blocks, kK4Threads, smem, stream>>>(frames, n, H, W, cuts, n_cuts, k,
-                                                                   H2, W2, rb, bands, slot, out,
-                                                                   index);
+  kern<<<(unsigned)blocks, kK4Threads, smem, stream>>>(frames, n, H, W, cuts, n_cuts, k, H2, W2, rb,
+                                                      bands, slot, out, index);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,8 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 from synth import manifest, torch_dev  # noqa: E402
 
+from nv12_helpers import random_nv12  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 
@@ -118,3 +120,24 @@ def test_sample_invalid(ctx, dev):
         ctx.sample_frames(fr, None, 0, 8, 8)
     with pytest.raises(ClipError):
         ctx.sample_frames(fr, None, 1, 8, 5000)
+
+
+@pytest.mark.parametrize("W,H,n,cuts,k,oh,ow", [
+    (1280, 720, 20, [9, 13], 3, 224, 224),
+    (854, 480, 12, [5], 2, 224, 224),
+    (1920, 1080, 6, [2], 2, 224, 224),
+    (64, 48, 8, [], 3, 96, 128),
+    (32, 16, 5, [1, 4], 2, 7, 9),
+])
+def test_sample_nv12_random_frames(ctx, dev, W, H, n, cuts, k, oh, ow):
+    """NV12 input: every tap converted by O0, then O11 — equal to the oracle's
+    resize of the oracle's full-frame conversion."""
+    rng = np.random.default_rng(W * 3 + H + n)
+    host = random_nv12(rng, n, H, W, structured=(W % 64 == 0))
+    rgb = np.stack([oracle.nv12_to_rgb(f) for f in host])
+    d = torch.from_numpy(host).to(dev)
+    c = torch.tensor(cuts, dtype=torch.int32, device=dev) if cuts else None
+    out, idx = ctx.sample_frames(d, c, k, oh, ow)
+    want, widx = oracle.sample_clips(rgb, cuts, k, oh, ow)
+    assert idx.cpu().numpy().tolist() == widx.tolist()
+    assert np.array_equal(out.cpu().numpy(), want)
