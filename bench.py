@@ -382,6 +382,19 @@ def run_ours(args):
             traffic = None
     fps = world * v.n / (ms_step * 1e-3)
     gbs = world * frame_bytes / (ms_step * 1e-3) / 1e9
+    # the binding resource of K1 is instruction issue: issue roofline
+    # = warp-instructions/s (ncu thread-instr/px of the committed capture x live px/s / 32)
+    # against 4 schedulers x 1 warp-instr/clk x SMs x the sampled SM clock
+    issue = None
+    clk_sum = clk.summary()
+    if instr_px and clk_sum.get("sm_mhz"):
+        px_s = v.n * v.npix / (k1_ms * 1e-3)
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_wi = n_sm * 4 * clk_sum["sm_mhz"] * 1e6
+        ach_wi = instr_px * px_s / 32.0
+        issue = {"bound": "issue", "achieved": round(ach_wi / 1e9, 1), "peak": round(peak_wi / 1e9, 1),
+                 "unit": "G warp-instr/s", "frac": round(ach_wi / peak_wi, 4),
+                 "thread_instr_per_px": instr_px, "sms": n_sm, "sm_mhz": clk_sum["sm_mhz"]}
 
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -414,13 +427,14 @@ def run_ours(args):
                      "alg_bytes_per_launch": k1_alg, "launch_ms": round(k1_ms, 4), "peak_src": peak_src,
                      "frac_of_read_ceiling": None if read_gbs is None else round(achieved / read_gbs, 4),
                      "frac_of_8tbs": round(achieved / 8000.0, 4), "instr_per_px_ncu": instr_px},
+        "roofline_issue": issue,
         "kernel_ms_per_step": {"k1": round(st["k1_ms"] / args.steps, 4),
                                "k2": round(st["k2_ms"] / args.steps, 4),
                                "k3": round(st["k3_ms"] / args.steps, 4)},
         "gpu_launches": int(st["launches"]),
         "per_rank_ms_per_step": [round(x, 4) for x in per_rank_ms],
         "gather_wall_ms_per_step_rank0": round(gather_ms, 4) if world > 1 else None,
-        "clocks": clk.summary(),
+        "clocks": clk_sum,
         "parity_vs_golden": parity,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -593,8 +607,13 @@ def run_shard_frames(args):
         v = manifest.subsample(v, args.frames)
     a, b = cdist.frame_shards(v.n, world)[rank]
     table = torch_dev.frame_table(v, dev)
-    frames = torch.empty((b - a, v.H, v.W, 3), dtype=torch.uint8, device=dev)
-    torch_dev.gen_frames(v, table, frames, t0=a, n=b - a)
+    nv12 = args.format == "nv12"
+    if nv12:
+        frames = torch.empty((b - a, v.H * 3 // 2, v.W), dtype=torch.uint8, device=dev)
+        torch_dev.gen_nv12(v, table, frames, t0=a, n=b - a)
+    else:
+        frames = torch.empty((b - a, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+        torch_dev.gen_frames(v, table, frames, t0=a, n=b - a)
     emb = torch.empty((b - a, manifest.EMB_DIM), dtype=torch.float32, device=dev)
     torch_dev.gen_emb(v, table, emb, t0=a, n=b - a)
     torch.cuda.synchronize()
@@ -632,7 +651,7 @@ def run_shard_frames(args):
     ms = max(per_rank)
     if rank == 0:
         parity = None
-        gpath = os.path.join(ROOT, "tests", "golden", "C2.json")
+        gpath = os.path.join(ROOT, "tests", "golden", "C2_NV12.json" if nv12 else "C2.json")
         if not args.frames and os.path.exists(gpath):
             g = json.load(open(gpath))["videos"][0]
             parity = out[0][0] == g["detected"] and out[0][1] == g["final"]
@@ -641,11 +660,13 @@ def run_shard_frames(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": "C2: ONE 10-min 720p video split by frame ranges over the GPUs (SURVEY f2)",
+            "config": {"workload": "C2: ONE 10-min 720p video split by frame ranges over the GPUs (SURVEY f2)"
+                                   + (", NV12 surfaces (f1)" if nv12 else ""),
+                       "format": args.format,
                        "frames": v.n, "frames_per_gpu": b - a,
                        "parallelism": f"frame-range sharding over {world} GPU(s); NCCL all-gathers of "
                                       "last histograms, L1 arrays and embeddings"},
-            "hbm_gbs": round(v.n * v.frame_bytes / (ms * 1e-3) / 1e9, 1),
+            "hbm_gbs": round(v.n * frames[0].numel() / (ms * 1e-3) / 1e9, 1),
             "per_rank_ms_per_step": [round(x, 4) for x in per_rank],
             "k1_ms_per_step_rank0": round(st["k1_ms"] / args.steps, 4),
             "phase_ms_rank0": dict(zip(["scan (K1+L1)", "seam (all-gather lasts, a4)",

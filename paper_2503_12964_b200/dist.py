@@ -111,7 +111,8 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
          video's L1 (identical detected cuts everywhere);
       4. all_gather of the embeddings -> clip_merge on the whole video.
     Results are identical to the single-GPU path (same kernels, same order).
-    `frames`: u8 cuda [m, H, W, 3] = frames f0..f0+m-1; `emb`: f32 cuda [m, D].
+    `frames`: u8 cuda [m, H, W, 3] (or NV12 [m, H*3/2, W]) = frames f0..f0+m-1;
+    `emb`: f32 cuda [m, D].
     `marks`: optional list; CUDA events recorded after each phase are appended
     (diagnosis of the exchange overhead).
     Returns (detected list, final list, cos tensor, band hits, rounds)."""
@@ -119,7 +120,12 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    m, H, W, _ = frames.shape
+    nv12 = frames.dim() == 3  # NV12 surfaces [m, H*3/2, W] (NEXT f1)
+    if nv12:
+        m, H3, W = frames.shape
+        H = H3 * 2 // 3
+    else:
+        m, H, W, _ = frames.shape
     dev = frames.device
     shards = frame_shards(n_total, world)
     width = max(b - a for a, b in shards)
@@ -139,7 +145,8 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
             marks.append(ev)
 
     mark()
-    hist, l1, _ = ctx.frame_scores(frames, want_score=False)
+    scores = ctx.frame_scores_nv12 if nv12 else ctx.frame_scores
+    hist, l1, _ = scores(frames, want_score=False)
     mark()
     nb = hist.shape[1]
     # (2) last histograms of every shard; the seam frame's L1 from histograms (K2 only)
