@@ -45,8 +45,12 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
                            {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
                            {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1},
-                           {4, 1, 16, 1, 3}, {4, 1, 16, 2, 2}};  // lut 2 = table without swizzle
-constexpr int kNumCfgs = 16;
+                           {4, 1, 16, 1, 3}, {4, 1, 16, 2, 2},  // lut 2 = table without swizzle
+                           {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3}};  // 5-deep ring; lut 3 = swizzle 2
+constexpr int kNumCfgs = 18;
+
+// table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2
+__host__ __device__ constexpr int lut_swz(int lut) { return lut == 1 ? 1 : (lut == 3 ? 2 : 0); }
 
 template <int STAGES, int LUT>
 struct K1Smem {
@@ -183,8 +187,8 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
   if constexpr (LUT) {
     uint32_t a0, a1, b0, b1;
-    const uint32_t p01 = code_pair_lut_pre<LUT == 1>(R01, G01, B01, mk, a0, a1);
-    const uint32_t p23 = code_pair_lut_pre<LUT == 1>(R23, G23, B23, mk, b0, b1);
+    const uint32_t p01 = code_pair_lut_pre<lut_swz(LUT)>(R01, G01, B01, mk, a0, a1);
+    const uint32_t p23 = code_pair_lut_pre<lut_swz(LUT)>(R23, G23, B23, mk, b0, b1);
     const uint32_t c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
     const uint32_t c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
     hist_inc(hb, lut_off_lo(c01, mk));
@@ -203,7 +207,7 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
 
 // NQ quads of one lane, phase by phase across all of them (loads, unpack,
 // codes, table lookups, atomics): NQ*2 independent pixel-pair chains in flight.
-template <int NQ>
+template <int NQ, int SWZ>
 __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qstride,
                                               uint32_t* hist, const uint8_t* lut, MadK mk) {
   uint32_t w[NQ][3];
@@ -219,8 +223,8 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
   for (int j = 0; j < NQ; ++j) {
     uint32_t R01, G01, B01, R23, G23, B23;
     unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
-    pre[2 * j] = code_pair_lut_pre<true>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-    pre[2 * j + 1] = code_pair_lut_pre<true>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    pre[2 * j] = code_pair_lut_pre<SWZ>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_lut_pre<SWZ>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
   }
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
@@ -264,7 +268,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       sm.c2b[i] = (uint8_t)(kUseLut ? code_to_bin_lut(i) : code_to_bin(i));
   if (kUseLut)
     for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ (LUT == 1 ? d : 0u);
+      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, lut_swz(LUT));
       sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
   if (tid == 0) {
@@ -349,7 +353,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       constexpr int kQPL = 4 * kStageGroups / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_lut<kQPL>(buf, tid, kConsumers, wh, sm.lut, mk);
+        bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, sm.lut, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
       }
@@ -449,6 +453,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
+    K1_CASE(16) K1_CASE(17)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -479,7 +484,9 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 12>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 13>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 14>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 15>();
+  if ((e = configure_cfg<MODE, 15>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 16>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 17>();
 }
 
 }  // namespace
