@@ -185,8 +185,8 @@ int k1_mode(const clip_params& p) {
   return (p.h_bins == 18 && p.s_bins == 3 && p.v_bins == 3) ? kModeFast : kModeGeneric;
 }
 
-int64_t stages_of(int64_t groups) {
-  const int64_t sg = k1_stage_groups();
+int64_t stages_of(int64_t groups, int cfg) {
+  const int64_t sg = k1_stage_groups(cfg);
   return (groups + sg - 1) / sg;
 }
 
@@ -194,7 +194,7 @@ int64_t stages_of(int64_t groups) {
 int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   int64_t total = 0;
   for (auto& s : segs) {
-    s.stages = stages_of(s.groups);
+    s.stages = stages_of(s.groups, ctx->k1_cfg);
     s.stage_base = total;
     total += s.n_frames * s.stages;
   }

@@ -27,8 +27,7 @@ namespace clipdetect {
 
 namespace {
 
-constexpr int kStageGroups = 512;  // 48-byte groups per stage (24 KiB), common to all configs
-constexpr int kStageBytes = kStageGroups * 48;
+constexpr int kStageGroups = 512;  // default 48-byte groups per stage (24 KiB)
 constexpr int kLutBytes = 65536;
 
 // Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
@@ -39,23 +38,25 @@ constexpr int kLutBytes = 65536;
 // noprod = no dedicated producer warp: the last consumer warp to release a
 // ring slot issues the slot's next TMA copy (lets a CTA hold 32 consumer warps).
 struct K1Cfg {
-  int stages, ctas_per_sm, warps, lut, quad, noprod = 0;
+  int stages, ctas_per_sm, warps, lut, quad, noprod = 0, sg = kStageGroups;  // sg: groups per stage
 };
 constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
                            {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
                            {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
                            {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1},
                            {4, 1, 16, 1, 3}, {4, 1, 16, 2, 2},  // lut 2 = table without swizzle
-                           {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3}};  // 5-deep ring; lut 3 = swizzle 2
-constexpr int kNumCfgs = 18;
+                           {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3},  // 5-deep ring; lut 3 = swizzle 2
+                           {3, 1, 16, 1, 3, 0, 768}, {2, 1, 16, 1, 3, 0, 1024},
+                           {4, 1, 16, 1, 3, 0, 640}};  // larger stages: fewer ring hand-offs
+constexpr int kNumCfgs = 21;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2
 __host__ __device__ constexpr int lut_swz(int lut) { return lut == 1 ? 1 : (lut == 3 ? 2 : 0); }
 
-template <int STAGES, int LUT>
+template <int STAGES, int LUT, int SG>
 struct K1Smem {
   static constexpr int kEntries = LUT ? kLutCodes : kCodes;
-  alignas(128) uint8_t buf[STAGES][kStageBytes];
+  alignas(128) uint8_t buf[STAGES][SG * 48];
   uint8_t lut[LUT ? kLutBytes : 16];
   uint32_t hist[kEntries];  // CTA-shared code (or bin) histogram
   uint32_t binacc[256];     // flush: per-bin sums
@@ -67,6 +68,7 @@ struct K1Smem {
 };
 
 // Walks the flattened (segment, frame, stage) space with 32-bit counters.
+template <int SG>
 struct StageIter {
   const HistSeg* segs;
   int32_t seg, frame, st;
@@ -79,7 +81,7 @@ struct StageIter {
     groups = g.groups;
     stages = (int32_t)g.stages;
     n_frames = (int32_t)g.n_frames;
-    last_ng = (int32_t)(g.groups - (g.stages - 1) * kStageGroups);
+    last_ng = (int32_t)(g.groups - (g.stages - 1) * SG);
     frames = g.frames;
   }
   __device__ void seek(const HistSeg* s, int32_t nseg, int64_t g) {
@@ -95,7 +97,7 @@ struct StageIter {
     frame = (int32_t)(rel / stages);
     st = (int32_t)(rel - (int64_t)frame * stages);
   }
-  __device__ __forceinline__ int32_t ng() const { return st == stages - 1 ? last_ng : kStageGroups; }
+  __device__ __forceinline__ int32_t ng() const { return st == stages - 1 ? last_ng : SG; }
   // advance; returns true if the frame (or segment) changed
   __device__ __forceinline__ bool next(bool more) {
     if (++st == stages) {
@@ -241,17 +243,17 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
   }
 }
 
-template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD>
+template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD, int SG>
 __global__ void __launch_bounds__(CW * 32 + (NOPROD ? 0 : 32), MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
   constexpr int kConsumers = CW * 32;
   constexpr int kThreads = kConsumers + (NOPROD ? 0 : 32);
-  constexpr int kGPT = kStageGroups / kConsumers;  // 0 when a stage has fewer groups than lanes
-  static_assert(kGPT == 0 || kGPT * kConsumers == kStageGroups, "stage must split evenly");
+  constexpr int kGPT = SG / kConsumers;  // 0 when a stage has fewer groups than lanes
+  static_assert(kGPT == 0 || kGPT * kConsumers == SG || QUAD, "stage must split evenly");
   constexpr bool kUseLut = (MODE == kModeFast) && LUT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  K1Smem<STAGES, LUT>& sm = *reinterpret_cast<K1Smem<STAGES, LUT>*>(smem_raw);
+  K1Smem<STAGES, LUT, SG>& sm = *reinterpret_cast<K1Smem<STAGES, LUT, SG>*>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t nbins = nh * ns * nv;
@@ -259,7 +261,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
 
-  constexpr int kEntries = K1Smem<STAGES, LUT>::kEntries;
+  constexpr int kEntries = K1Smem<STAGES, LUT, SG>::kEntries;
   const uint32_t nentries = MODE == kModeFast ? (uint32_t)kEntries : nbins;
   for (int i = tid; i < kEntries; i += kThreads) sm.hist[i] = 0u;
   for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
@@ -285,7 +287,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 
   // noprod: the first STAGES copies come from thread 0; `ahead` tracks the stage
   // a slot is refilled with (i + STAGES) in every warp
-  StageIter ahead;
+  StageIter<SG> ahead;
   uint64_t pol = 0;
   if constexpr (NOPROD) {
     pol = policy_evict_first();
@@ -294,7 +296,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     for (int32_t i = 0; i < STAGES && i < n; ++i) {
       if (tid == 0) {
         const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
-        const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * kStageGroups) * 48;
+        const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * SG) * 48;
         mbar_arrive_expect_tx(&sm.full[i], bytes);
         bulk_g2s(sm.buf[i], src, bytes, &sm.full[i], pol);
       }
@@ -306,14 +308,14 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     // ---------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      StageIter it;
+      StageIter<SG> it;
       it.seek(segs, nseg, s_begin);
       const int32_t n = (int32_t)(s_end - s_begin);
       uint32_t slot = 0, par = 0;
       for (int32_t i = 0; i < n; ++i) {
         if (i >= STAGES) mbar_wait(&sm.empty[slot], par ^ 1u);
         const uint32_t bytes = (uint32_t)it.ng() * 48u;
-        const uint8_t* src = it.frames + ((int64_t)it.frame * it.groups + (int64_t)it.st * kStageGroups) * 48;
+        const uint8_t* src = it.frames + ((int64_t)it.frame * it.groups + (int64_t)it.st * SG) * 48;
         mbar_arrive_expect_tx(&sm.full[slot], bytes);
         bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
         it.next(i + 1 < n);
@@ -337,7 +339,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   }
   uint32_t* wh = sm.hist;
   uint32_t xacc = 0;
-  StageIter it;
+  StageIter<SG> it;
   it.seek(segs, nseg, s_begin);
   const int32_t n = (int32_t)(s_end - s_begin);
   uint32_t slot = 0, par = 0;
@@ -350,7 +352,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 #pragma unroll 2
       for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
     } else if constexpr (QUAD == 3 && MODE == kModeFast && LUT) {
-      constexpr int kQPL = 4 * kStageGroups / kConsumers;
+      constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
         bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, sm.lut, mk);
@@ -359,7 +361,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       }
     } else if constexpr (QUAD == 2 && MODE == kModeFast) {
       // all of a lane's quads of a full stage issued together (more independent work per warp)
-      constexpr int kQPL = 4 * kStageGroups / kConsumers;
+      constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
 #pragma unroll
@@ -384,7 +386,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
         if (i + STAGES < n) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
-          const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * kStageGroups) * 48;
+          const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * SG) * 48;
           mbar_arrive_expect_tx(&sm.full[slot], bytes);
           bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
         }
@@ -429,10 +431,10 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 template <int MODE, int C>
 struct Cfg {
   static constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm, W = kCfgs[C].warps,
-                       L = kCfgs[C].lut, Q = kCfgs[C].quad, NP = kCfgs[C].noprod;
+                       L = kCfgs[C].lut, Q = kCfgs[C].quad, NP = kCfgs[C].noprod, G = kCfgs[C].sg;
   static constexpr int kThreads = W * 32 + (NP ? 0 : 32);
-  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q, NP>; }
-  static constexpr size_t smem() { return sizeof(K1Smem<S, L>); }
+  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q, NP, G>; }
+  static constexpr size_t smem() { return sizeof(K1Smem<S, L, G>); }
 };
 
 template <int MODE, int C>
@@ -453,7 +455,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
-    K1_CASE(16) K1_CASE(17)
+    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -486,12 +488,15 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 14>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 15>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 16>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 17>();
+  if ((e = configure_cfg<MODE, 17>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 18>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 19>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 20>();
 }
 
 }  // namespace
 
-int k1_stage_groups() { return kStageGroups; }
+int k1_stage_groups(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].sg : kStageGroups; }
 int k1_num_cfgs() { return kNumCfgs; }
 
 cudaError_t k1_configure() {

@@ -11,7 +11,7 @@ namespace clipdetect {
 enum { kModeFast = 0, kModeGeneric = 1, kModeRead = 2 };
 
 // ---- K1 (hist.cu)
-int k1_stage_groups();
+int k1_stage_groups(int cfg);  // 48-byte groups per K1 stage of a launch configuration
 int k1_num_cfgs();
 cudaError_t k1_configure();
 int k1_grid(int cfg, int sm_count, int64_t total_stages);
