@@ -19,6 +19,8 @@
 //  * at a frame change the code histogram is mapped to the 162 bins
 //    (code_to_bin, a 2 KB smem table) and added to the global u32 histogram
 //    (integer adds: order-free, bit-deterministic).
+#include <stddef.h>
+
 #include "binfn.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -28,6 +30,7 @@ namespace clipdetect {
 namespace {
 
 constexpr int kStageGroups = 512;  // default 48-byte groups per stage (24 KiB)
+constexpr uint32_t kDynSmemBase = 0x400;  // shared-window offset of dynamic smem (after 1 KiB system reserve)
 constexpr int kLutBytes = 65536;
 
 // Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
@@ -211,7 +214,7 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
 // codes, table lookups, atomics): NQ*2 independent pixel-pair chains in flight.
 template <int NQ, int SWZ>
 __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qstride,
-                                              uint32_t* hist, const uint8_t* lut, MadK mk) {
+                                              uint32_t* hist, uint32_t lut_s, MadK mk) {
   uint32_t w[NQ][3];
 #pragma unroll
   for (int j = 0; j < NQ; ++j) {
@@ -231,8 +234,8 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
-    qa[j] = lut[ia[j]];
-    qb[j] = lut[ib[j]];
+    qa[j] = lds_u8(lut_s + ia[j]);
+    qb[j] = lds_u8(lut_s + ib[j]);
   }
   char* hb = reinterpret_cast<char*>(hist);
 #pragma unroll
@@ -260,6 +263,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 
   const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
+  if ((uint32_t)__cvta_generic_to_shared(smem_raw) != kDynSmemBase) __trap();  // see lut_s
 
   constexpr int kEntries = K1Smem<STAGES, LUT, SG>::kEntries;
   const uint32_t nentries = MODE == kModeFast ? (uint32_t)kEntries : nbins;
@@ -338,6 +342,12 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t* wh = sm.hist;
+  using Smem = K1Smem<STAGES, LUT, SG>;
+  // The hue table's 32-bit shared-window address as a compile-time constant:
+  // dynamic shared memory starts after the 1 KiB the system reserves, at
+  // kDynSmemBase, for a launch without clusters (checked at kernel entry), so
+  // each table load is LDS [index + imm] with no per-load base add.
+  constexpr uint32_t lut_s = kDynSmemBase + (uint32_t)offsetof(Smem, lut);
   uint32_t xacc = 0;
   StageIter<SG> it;
   it.seek(segs, nseg, s_begin);
@@ -355,7 +365,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, sm.lut, mk);
+        bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
       }

@@ -25,6 +25,8 @@
 // Fast path: 18x3x3 bins, W % 16 == 0, W <= 8192.  Anything else runs the
 // plain generic kernel at the bottom of this file (same conversion, direct
 // global loads, bin_generic).
+#include <stddef.h>
+
 #include <algorithm>
 
 #include "binfn.cuh"
@@ -110,9 +112,13 @@ __device__ __forceinline__ void block_chroma(uint32_t uv, int k, int32_t& ruv, i
   nv12_chroma(U, V, ruv, guv, buv);
 }
 
+// Shared-window offset of dynamic shared memory (after the 1 KiB system
+// reserve) for a launch without clusters, checked at kernel entry: the table
+// loads become LDS [index + imm] with no per-load base add.
+constexpr uint32_t kNvDynSmemBase = 0x400;
+
 // One 2 x 8 tile: Y row 0 (y0), Y row 1 (y1), UV (c): 8 pixel pairs.
-__device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, const uint8_t* lut,
-                                        MadK mk) {
+__device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, MadK mk) {
   uint32_t pre[8], ia[8], ib[8];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -130,10 +136,11 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, c
     }
   }
   uint32_t qa[8], qb[8];
+  constexpr uint32_t lut_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem, lut);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    qa[j] = lut[ia[j]];
-    qb[j] = lut[ib[j]];
+    qa[j] = lds_u8(lut_s + ia[j]);
+    qb[j] = lds_u8(lut_s + ib[j]);
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -155,6 +162,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
 
   const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
+  if ((uint32_t)__cvta_generic_to_shared(smem_raw) != kNvDynSmemBase) __trap();  // see nv_tile
 
   if (MODE == kModeFast) {
     for (int i = tid; i < kLutCodes; i += blockDim.x) {
@@ -245,7 +253,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       if constexpr (MODE == kModeRead) {
         xacc ^= a.x ^ a.y ^ b.x ^ b.y ^ c.x ^ c.y;
       } else {
-        nv_tile(a, b, c, hb, sm.lut, mk);
+        nv_tile(a, b, c, hb, mk);
       }
       cx += dr;
       br += dq;
