@@ -99,12 +99,21 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.05)
+        # NVML initialisation can take longer than a short timed region: wait
+        # for the sampler's first reading before the region starts
+        t0 = time.time()
+        while not self.sm and time.time() - t0 < 10.0 and self._t.is_alive():
+            time.sleep(0.005)
+        self._n0 = len(self.sm)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        # keep the readings taken inside the region (the last pre-region one if
+        # the region was shorter than one period)
+        n0 = max(0, getattr(self, "_n0", 1) - 1)
+        self.sm, self.mx = self.sm[n0:], self.mx[n0:]
 
     def summary(self):
         if not self.sm:
