@@ -200,17 +200,24 @@ CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
 // the lookups of a warp on smooth content (d, na jittering by +-1 around a few
 // values, e.g. decoded NV12 where the luma noise moves r, g, b together)
 // nearly conflict-free (bank-conflict simulation in DESIGN.md §7).
+// 3: (na + 4d) mod 256 — the same bank spread as 2 (bank = (na/4 + d) mod 32,
+// up to a carry) but computed by one IMAD on the FMA pipe instead of a LOP3 on
+// the busier ALU pipe (the mod 256 is free: the index PRMT takes the low byte).
 CD_HD uint32_t lut_swizzle(uint32_t d, int swz) {
   return swz == 2 ? ((d << 2) & 0xFCu) : (swz == 1 ? d : 0u);
 }
-CD_HD uint32_t lut_index(uint32_t na, uint32_t d, int swz = 1) {
-  return d * 256u + (na ^ lut_swizzle(d, swz));
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d, int swz = 3) {
+  return d * 256u + (swz == 3 ? ((na + 4u * d) & 255u) : (na ^ lut_swizzle(d, swz)));
+}
+// inverse: the na stored at byte b of row d
+CD_HD uint32_t lut_unswizzle(uint32_t b, uint32_t d, int swz) {
+  return swz == 3 ? ((b - 4u * d) & 255u) : (b ^ lut_swizzle(d, swz));
 }
 
 // Part 1 (before the table lookups): returns the partial code and the two
 // lanes' table indices.  The sector is carried as the three raw ordering
 // flags A, B, C (parity is decoded from them in code_to_bin_lut).
-template <int SWZ = 1>
+template <int SWZ = 3>
 CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   constexpr uint32_t kB15 = 0x80008000u;
@@ -220,9 +227,10 @@ CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t sum = cd_mad(B, k.one, cd_mad(R, k.one, G));
   const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, sum));  // mid - min
   // bank swizzle (lut_swizzle, both lanes at once)
-  const uint32_t nas = SWZ == 2 ? (na ^ (cd_mad(d, 4u, 0u) & 0x00FC00FCu)) : (SWZ == 1 ? (na ^ d) : na);
-  i0 = cd_prmt(nas, d, 0x1140u);  // lane 0: nas | d << 8
-  i1 = cd_prmt(nas, d, 0x3362u);  // lane 1
+  const uint32_t nas = SWZ == 3 ? cd_mad(d, 4u, na)  // lanes stay < 2^16: no carry between them
+                       : SWZ == 2 ? (na ^ (cd_mad(d, 4u, 0u) & 0x00FC00FCu)) : (SWZ == 1 ? (na ^ d) : na);
+  i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8 (bytes 2-3 from d: zero)
+  i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
   const uint32_t R15 = cd_mad(R, k.one, kB15);
   const uint32_t tA = cd_mad(G, k.neg1, R15);  // bit 15: r >= g   (IMAD)
   const uint32_t tB = G + kB15 - B;            // bit 15: g >= b   (IADD3)

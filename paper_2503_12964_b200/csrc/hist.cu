@@ -50,11 +50,14 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {4, 1, 16, 1, 3}, {4, 1, 16, 2, 2},  // lut 2 = table without swizzle
                            {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3},  // 5-deep ring; lut 3 = swizzle 2
                            {3, 1, 16, 1, 3, 0, 768}, {2, 1, 16, 1, 3, 0, 1024},
-                           {4, 1, 16, 1, 3, 0, 640}};  // larger stages: fewer ring hand-offs
-constexpr int kNumCfgs = 21;
+                           {4, 1, 16, 1, 3, 0, 640},  // larger stages: fewer ring hand-offs
+                           {4, 1, 16, 4, 3}};  // lut 4 = swizzle 3 (IMAD instead of LOP3)
+constexpr int kNumCfgs = 22;
 
-// table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2
-__host__ __device__ constexpr int lut_swz(int lut) { return lut == 1 ? 1 : (lut == 3 ? 2 : 0); }
+// table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
+__host__ __device__ constexpr int lut_swz(int lut) {
+  return lut == 1 ? 1 : (lut == 3 ? 2 : (lut == 4 ? 3 : 0));
+}
 
 template <int STAGES, int LUT, int SG>
 struct K1Smem {
@@ -148,8 +151,8 @@ __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, co
       uint32_t c01, c23;
       if (LUT) {
         uint32_t a0, a1, b0, b1;
-        const uint32_t p01 = code_pair_lut_pre(R01, G01, B01, mk, a0, a1);
-        const uint32_t p23 = code_pair_lut_pre(R23, G23, B23, mk, b0, b1);
+        const uint32_t p01 = code_pair_lut_pre<lut_swz(LUT)>(R01, G01, B01, mk, a0, a1);
+        const uint32_t p23 = code_pair_lut_pre<lut_swz(LUT)>(R23, G23, B23, mk, b0, b1);
         c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
         c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
       } else {
@@ -274,7 +277,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       sm.c2b[i] = (uint8_t)(kUseLut ? code_to_bin_lut(i) : code_to_bin(i));
   if (kUseLut)
     for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, lut_swz(LUT));
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, lut_swz(LUT));
       sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
   if (tid == 0) {
@@ -465,7 +468,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
-    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20)
+    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -501,7 +504,8 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 17>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 18>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 19>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 20>();
+  if ((e = configure_cfg<MODE, 20>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 21>();
 }
 
 }  // namespace
@@ -547,7 +551,7 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
   extern __shared__ __align__(16) uint8_t lut[];
   if (LUT) {
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ d;
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, 3);
       lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
     __syncthreads();

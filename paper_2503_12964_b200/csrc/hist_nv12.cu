@@ -42,7 +42,7 @@ constexpr int kNvStageBytes = 24576;  // 3 * R * W <= 24576  <=>  R * W <= 8192
 constexpr int kNvWarps = 16;
 constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvLutBytes = 65536;
-constexpr int kNvSwz = 2;  // table swizzle (binfn.cuh lut_swizzle): conflict-free rows on NV12 content
+constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-free rows on NV12 content
 
 struct NvSmem {
   alignas(128) uint8_t buf[kNvStages][kNvStageBytes];
@@ -171,7 +171,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     }
     for (int i = tid; i < 256; i += blockDim.x) sm.binacc[i] = 0u;
     for (int i = tid; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, kNvSwz);
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
       sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
   }
@@ -357,7 +357,7 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
   extern __shared__ __align__(16) uint8_t lut[];
   if (FAST) {
     for (int i = threadIdx.x; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = ((uint32_t)i & 255u) ^ lut_swizzle(d, kNvSwz);
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
       lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
     }
     __syncthreads();

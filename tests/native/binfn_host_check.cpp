@@ -22,10 +22,18 @@ int main(int argc, char** argv) {
   std::vector<uint8_t> t0(N), t1(N), tg(N), l0(N), l1(N);
   std::vector<uint8_t> lut(65536, 0);
   for (uint32_t d = 0; d < 256; ++d)
-    for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d)] = (uint8_t)lut_entry(na, d);
-  std::vector<uint8_t> lut2(65536, 0);  // swizzle 2 (the NV12 kernel's table)
+    for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d, 1)] = (uint8_t)lut_entry(na, d);  // K1 cfg14
+  std::vector<uint8_t> lut2(65536, 0);  // swizzle 3 (the NV12 kernel's table)
   for (uint32_t d = 0; d < 256; ++d)
-    for (uint32_t na = 0; na <= d; ++na) lut2[lut_index(na, d, 2)] = (uint8_t)lut_entry(na, d);
+    for (uint32_t na = 0; na <= d; ++na) lut2[lut_index(na, d, 3)] = (uint8_t)lut_entry(na, d);
+  // the unswizzle used by the kernels' table initialisation inverts every swizzle
+  for (int swz = 0; swz <= 3; ++swz)
+    for (uint32_t d = 0; d < 256; ++d)
+      for (uint32_t na = 0; na < 256; ++na)
+        if (lut_unswizzle(lut_index(na, d, swz) & 255u, d, swz) != na) {
+          fprintf(stderr, "lut_unswizzle mismatch swz %d\n", swz);
+          return 1;
+        }
   for (uint32_t c = 0; c < N; ++c) {
     const uint32_t c2 = c ^ 0xA5A5A5u;
     const uint32_t R = (c >> 16) | ((c2 >> 16) << 16);
@@ -36,7 +44,7 @@ int main(int argc, char** argv) {
     t1[c2] = (uint8_t)code_to_bin(code_off_hi(code, kMadK) >> 2);
     tg[c] = (uint8_t)bin_generic(c >> 16, (c >> 8) & 255u, c & 255u, nh, ns, nv);
     uint32_t i0, i1;
-    const uint32_t pre = code_pair_lut_pre(R, G, B, kMadK, i0, i1);
+    const uint32_t pre = code_pair_lut_pre<1>(R, G, B, kMadK, i0, i1);
     const uint32_t lc = code_pair_lut_post(pre, lut[i0], lut[i1], kMadK);
     l0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
     l1[c2] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);
@@ -76,7 +84,7 @@ int main(int argc, char** argv) {
     uint32_t R, G, B;
     nv12_pair_rgb(Y, Y2, ruv, guv, buv, R, G, B);
     uint32_t i0, i1;
-    const uint32_t pre = code_pair_lut_pre<2>(R, G, B, kMadK, i0, i1);
+    const uint32_t pre = code_pair_lut_pre<3>(R, G, B, kMadK, i0, i1);
     const uint32_t lc = code_pair_lut_post(pre, lut2[i0], lut2[i1], kMadK);
     n0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
     n1[(Y2 << 16) | (U << 8) | V] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);

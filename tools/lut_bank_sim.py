@@ -20,6 +20,7 @@ def idx_of(d, na, swz):
     if swz == 'xor': return d * 256 + (na ^ d)
     if swz == 'none': return d * 256 + na
     if swz == 'xor4': return d * 256 + ((na ^ (d << 2)) & 255)
+    if swz == 'add4': return d * 256 + ((na + 4 * d) & 255)
 def wavefronts(idx):  # idx: [n_instr, 32] byte indices
     words = idx >> 2
     bank = words & 31
@@ -57,7 +58,7 @@ def rgb_instrs(rgb, swz, n=4000):
         out.append(idx_of(dflat[f, px], naflat[f, px], swz))
     return np.array(out)
 noise = rng.integers(0, 256, (2, H, W, 3)).astype(np.int32)
-for swz in ['xor', 'none', 'xor4']:
+for swz in ['xor', 'none', 'xor4', 'add4']:
     print(swz, 'NV12-c2', round(wavefronts(nv12_instrs(rgbs, swz)), 2), 'RGB-c2', round(wavefronts(rgb_instrs(rgb_direct, swz)), 2),
           'RGB-noise', round(wavefronts(rgb_instrs(noise, swz)), 2))
 def nv12_instrs4(rgb, swz, n=4000):
