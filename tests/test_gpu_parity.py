@@ -439,3 +439,39 @@ def test_c2_full_through_per_step_api_in_chunks(ctx, dev):
     assert merged.cpu().numpy().tolist() == g["final"]
     np.testing.assert_allclose(cos.cpu().numpy(), np.array(g["cos"]), rtol=COS_RTOL, atol=1e-12)
     assert hits == g["n_band_hits"] and rounds == g["rounds"]
+
+
+def test_8k_frames_rgb_and_nv12(ctx, dev):
+    """Maximum-size frames of practical video (7680x4320, 99.5 MB RGB24): K1 and
+    K1-NV12 (one frame spans ~4,050 stages, many CTAs per frame) equal the oracle."""
+    rng = np.random.default_rng(8)
+    H, W = 4320, 7680
+    rgb = rng.integers(0, 256, (2, H, W, 3), dtype=np.uint8)
+    rgb[1, : H // 2] = rgb[0, : H // 2]  # half the second frame repeats the first
+    hist, l1, _ = ctx.frame_scores(torch.from_numpy(rgb).to(dev))
+    want = oracle.hist_frames(rgb)
+    assert np.array_equal(_u32(hist), want)
+    assert np.array_equal(_u32(l1), oracle.l1(want, H * W)[0])
+    del rgb
+    from nv12_helpers import random_nv12
+    nv = random_nv12(rng, 2, H, W)
+    hist, l1, _ = ctx.frame_scores_nv12(torch.from_numpy(nv).to(dev))
+    want = oracle.hist_nv12_frames(nv)
+    assert np.array_equal(_u32(hist), want)
+    torch.cuda.empty_cache()
+
+
+def test_frame_count_limit_rejected_before_any_work(ctx, dev):
+    """A batch of more than INT32_MAX frames is refused by validation (nothing is
+    allocated, generated or launched: the fill callback is never called)."""
+    from paper_2503_12964_b200 import ClipError
+    called = []
+
+    def fill(*a):
+        called.append(a)
+        return 1
+
+    vids = [{"n": (1 << 30), "H": 16, "W": 16, "frames": None, "emb": None} for _ in range(3)]
+    with pytest.raises(ClipError) as e:
+        ctx.run_videos(vids, fill=fill)
+    assert e.value.code == 1 and not called
