@@ -6,4 +6,4 @@ colour-change cuts, and the embedding-similarity merge, as hand-written
 sm_100a CUDA kernels behind a C ABI (include/clip_detect.h).
 """
 from ._build import build  # noqa: F401
-from .clipdetect import (Ctx, ClipError, default_params, load)  # noqa: F401
+from .clipdetect import (Ctx, ClipError, default_params, load, run)  # noqa: F401

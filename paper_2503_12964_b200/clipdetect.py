@@ -359,3 +359,30 @@ class Ctx:
     def debug_read_roofline_nv12(self, frames):
         n, H3, W = frames.shape
         self._check(self._lib.clip_debug_read_roofline_nv12(self._h, _ptr(frames), n, H3 * 2 // 3, W))
+
+
+_run_ctx = {}
+
+
+def run(frames, emb=None, params: ClipParams | None = None, want_detected: bool = False):
+    """One video through rows a1-a9 (SURVEY.md §8(b) "Python shell"):
+    ``frames`` u8 cuda [T, H, W, 3] (RGB24) or [T, H*3/2, W] (NV12), ``emb`` f32
+    cuda [T, D] or None (no merge).  Uses a cached Ctx per (device, params) on the
+    current stream.  Returns the final cut list (and the detected cuts if
+    ``want_detected``)."""
+    import torch
+    dev = frames.device.index or 0
+    key = (dev, None if params is None else bytes(params))
+    ctx = _run_ctx.get(key)
+    if ctx is None or ctx.stream != torch.cuda.current_stream(dev):
+        ctx = Ctx(params, device=dev)
+        _run_ctx[key] = ctx
+    nv12 = frames.dim() == 3
+    T = frames.shape[0]
+    H = frames.shape[1] * 2 // 3 if nv12 else frames.shape[1]
+    W = frames.shape[2]
+    item = {"n": T, "H": H, "W": W, "frames": frames, "emb": emb,
+            "format": FORMAT_NV12 if nv12 else FORMAT_RGB24}
+    r = ctx.run_videos([item])[0]
+    fin = [int(x) for x in r.final]
+    return (fin, [int(x) for x in r.detected]) if want_detected else fin

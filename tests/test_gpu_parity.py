@@ -475,3 +475,15 @@ def test_frame_count_limit_rejected_before_any_work(ctx, dev):
     with pytest.raises(ClipError) as e:
         ctx.run_videos(vids, fill=fill)
     assert e.value.code == 1 and not called
+
+
+def test_python_shell_run(dev):
+    """clipdetect.run (SURVEY §8(b) Python shell) on C1: RGB and NV12."""
+    from paper_2503_12964_b200 import run
+    v = manifest.c1_video()
+    frames, emb = _dev_video(v, dev)
+    fin, det = run(frames, emb, want_detected=True)
+    assert fin == [10, 32, 53] and det == [10, 21, 32, 43, 53]
+    nv = torch.from_numpy(synth.gen_nv12(v)).to(dev)
+    assert run(nv, emb) == [10, 32, 53]
+    assert run(frames) == [10, 21, 32, 43, 53]  # no embeddings: no merge
