@@ -37,6 +37,7 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
+  int nv12_dir = 1;  // K1-NV12 code layout: 1 = direct offsets, 0 = LUT codes (CLIPDETECT_NV12_DIR)
   int k1_cfg = 14;  // K1 launch configuration: LUT hue, staged lane-contiguous quads, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
@@ -243,7 +244,7 @@ int launch_k1_nv12(clip_ctx* ctx, const std::vector<Nv12Seg>& all, int mode) {
     Span sp(ctx, 0);
     CK(k1_nv12_launch(k ? kModeGeneric : mode, P<Nv12Seg>(db), (int32_t)segs.size(), total,
                       p.h_bins, p.s_bins, p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count,
-                      ctx->stream));
+                      ctx->nv12_dir, ctx->stream));
     sp.end();
     ctx->stats.k1_launches += 1;
     ctx->stats.launches += 1;
@@ -452,6 +453,7 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
     const int c = atoi(e);
     if (c >= 0 && c < k1_num_cfgs()) ctx->k1_cfg = c;
   }
+  if (const char* e = getenv("CLIPDETECT_NV12_DIR")) ctx->nv12_dir = atoi(e) ? 1 : 0;
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       k1_nv12_configure() != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -936,7 +938,7 @@ int clip_debug_nv12map(clip_ctx* ctx, uint8_t* table) {
   CKS(check_ctx(ctx));
   if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
   CK(k5_nv12map_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
-                       k1_mode(ctx->p) == kModeFast, ctx->stream));
+                       k1_mode(ctx->p) == kModeFast, ctx->nv12_dir, ctx->stream));
   ctx->stats.launches += 1;
   return CLIP_OK;
 }

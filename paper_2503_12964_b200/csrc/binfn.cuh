@@ -112,8 +112,10 @@ struct MadK {
   uint32_t sl4;   // 2^4
   uint32_t sl16;  // 2^16
   uint32_t sl20;  // 2^20
+  uint32_t four, neg4, neg6;
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20,
+                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -262,6 +264,79 @@ CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
   const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
   const uint32_t oidx = (A << 2) | (B << 1) | C;
   if (z || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
+  if (qr == 0u && qf == 0u) return oidx == 7u ? v : 255u;  // grey (d = 0): h = 0, s = 0
+  const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
+  return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
+}
+
+// ------------------------------------------------------------ direct-offset variant
+// Each lane's code IS the byte offset of its code-histogram entry, so nothing
+// runs between the table lookup and the shared-memory atomic but one PRMT:
+//   offset = byte1 << 8 | byte0,
+//   byte0 = the table entry (qr | qf << 2) << 2   (bits 2-5; bits 0-1, 6-7 zero),
+//   byte1 = v (bits 8-9) | s1 (10) | s2 (11) | A = [r>=g] (12) | B = [g>=b] (13)
+//           | C = [r>=b] (14) | 0 (15)          -> offsets < 0x8000: 8192 entries.
+// The byte-1 fields are threshold bits (a - b + 2^j, see code_pair) merged by
+// bit-selects: every select takes ONE field from its source and keeps the rest,
+// and the field values never carry into bit 15.  The table index is the
+// swizzle-3 index (na + 4d) mod 256, computed straight from the channel sum:
+//   na + 4d = (r + g + b) + 3 max - 6 min   (mid = sum - max - min).
+constexpr int kDirCodes = 8192;
+CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d) { return lut_entry(na, d) << 2; }
+
+// bit select (a where m, else b) as ONE LOP3: written as inline PTX so that the
+// compiler does not flatten a chain of selects into and-or terms (one more op)
+template <uint32_t M>
+CD_HD uint32_t cd_sel(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(M));
+  return r;
+#else
+  return (a & M) | (b & ~M);
+#endif
+}
+
+// Part 1: byte 1 of both lanes' offsets (in bytes 1 and 3 of the result) and
+// the two table indices.  TBF = 1 computes B on the FMA pipe (two IMADs)
+// instead of one IADD3 on the ALU pipe.
+template <int TBF = 0>
+CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
+                                 uint32_t& i1) {
+  const uint32_t mx = cd_max3_u16x2(R, G, B);
+  const uint32_t mn = cd_min3_u16x2(R, G, B);
+  const uint32_t d = cd_mad(mn, k.neg1, mx);
+  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, k.three, R)));
+  const uint32_t nas = cd_mad(mn, k.neg6, t);  // na + 4d; lanes in [0, 1275]
+  i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8
+  i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
+  const uint32_t tA = R + 0x10001000u - G;  // bit 12: r >= g   (IADD3)
+  const uint32_t tB = TBF ? cd_mad(B, k.neg1, cd_mad(G, k.one, 0x20002000u))
+                          : G + 0x20002000u - B;                       // bit 13: g >= b
+  const uint32_t tC = cd_mad(B, k.neg4, cd_mad(R, k.four, 0x40004000u));  // bit 14: r >= b
+  const uint32_t z1 = cd_mad(mx, k.neg1, 0x04000400u);
+  const uint32_t x1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10:  bit 10 = s1, < 2^11
+  const uint32_t x2 = cd_mad(z1, k.one, x1);   // 3d - 2mx + 2^11: bit 11 = s2, < 2^12
+  const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8-9 of 3 max = v, < 2^10
+  uint32_t p = cd_sel<0x04000400u>(x1, x2);  // bit 10 s1, bit 11 s2, bits 12-15 zero
+  p = cd_sel<0x03000300u>(m3, p);
+  p = cd_sel<0x10001000u>(tA, p);
+  p = cd_sel<0x20002000u>(tB, p);
+  return cd_sel<0x40004000u>(tC, p);
+}
+// Part 2: the two lanes' byte offsets from the looked-up entries q0, q1 (u8).
+CD_HD uint32_t dir_off_lo(uint32_t pre, uint32_t q0) { return cd_prmt(q0, pre, 0x1150u); }
+CD_HD uint32_t dir_off_hi(uint32_t pre, uint32_t q1) { return cd_prmt(q1, pre, 0x1170u); }
+
+// code index (byte offset / 4) -> bin in [0,162), or 255 for an unreachable code.
+CD_HD uint32_t code_to_bin_dir(uint32_t idx) {
+  const uint32_t c = idx << 2;
+  const uint32_t qr = (c >> 2) & 3u, qf = (c >> 4) & 3u, z = (c >> 6) & 3u, v = (c >> 8) & 3u;
+  const uint32_t s1 = (c >> 10) & 1u, s2 = (c >> 11) & 1u, A = (c >> 12) & 1u;
+  const uint32_t B = (c >> 13) & 1u, C = (c >> 14) & 1u, z2 = c >> 15;
+  const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
+  const uint32_t oidx = (A << 2) | (B << 1) | C;
+  if (z || z2 || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
   if (qr == 0u && qf == 0u) return oidx == 7u ? v : 255u;  // grey (d = 0): h = 0, s = 0
   const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
   return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;

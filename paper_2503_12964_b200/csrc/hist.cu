@@ -51,17 +51,23 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3},  // 5-deep ring; lut 3 = swizzle 2
                            {3, 1, 16, 1, 3, 0, 768}, {2, 1, 16, 1, 3, 0, 1024},
                            {4, 1, 16, 1, 3, 0, 640},  // larger stages: fewer ring hand-offs
-                           {4, 1, 16, 4, 3}};  // lut 4 = swizzle 3 (IMAD instead of LOP3)
-constexpr int kNumCfgs = 22;
+                           {4, 1, 16, 4, 3},   // lut 4 = swizzle 3 (IMAD instead of LOP3)
+                           {4, 1, 16, 5, 3}, {4, 1, 16, 6, 3},  // lut 5/6 = direct offsets
+                           {4, 1, 16, 5, 4},   // quad 4 = lane-contiguous octets (LDS.64)
+                           {4, 1, 8, 5, 3}, {3, 1, 16, 5, 3, 0, 768},  // fewer ring hand-offs per pixel
+                           {3, 1, 16, 5, 4, 0, 768}};
+constexpr int kNumCfgs = 28;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
-  return lut == 1 ? 1 : (lut == 3 ? 2 : (lut == 4 ? 3 : 0));
+  return lut == 1 ? 1 : (lut == 3 ? 2 : (lut >= 4 ? 3 : 0));
 }
+// lut 5 / 6: direct-offset codes (binfn.cuh code_pair_dir_pre; 6 = B on the FMA pipe)
+__host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
 
 template <int STAGES, int LUT, int SG>
 struct K1Smem {
-  static constexpr int kEntries = LUT ? kLutCodes : kCodes;
+  static constexpr int kEntries = lut_dir(LUT) ? kDirCodes : (LUT ? kLutCodes : kCodes);
   alignas(128) uint8_t buf[STAGES][SG * 48];
   uint8_t lut[LUT ? kLutBytes : 16];
   uint32_t hist[kEntries];  // CTA-shared code (or bin) histogram
@@ -130,6 +136,16 @@ __device__ __forceinline__ void hist_inc(char* hb, uint32_t off) {
   atomicAdd(reinterpret_cast<uint32_t*>(hb + off), 1u);
 }
 #endif
+// the same increment at a shared-window address given as register + constant
+// (ATOMS [R + imm]: no per-atomic base add)
+template <uint32_t BASE>
+__device__ __forceinline__ void hist_inc_s(uint32_t off) {
+#ifdef CLIPDETECT_EXP_NO_ATOMS
+  if (off == 0xFFFFFFFFu) g_exp_sink = off;
+#else
+  asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(off), "n"(BASE) : "memory");
+#endif
+}
 
 template <int MODE, int LUT>
 __device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, const uint8_t* lut,
@@ -193,7 +209,15 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   char* hb = reinterpret_cast<char*>(hist);
   uint32_t R01, G01, B01, R23, G23, B23;
   unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
-  if constexpr (LUT) {
+  if constexpr (lut_dir(LUT)) {
+    uint32_t a0, a1, b0, b1;
+    const uint32_t p01 = code_pair_dir_pre<LUT == 6>(R01, G01, B01, mk, a0, a1);
+    const uint32_t p23 = code_pair_dir_pre<LUT == 6>(R23, G23, B23, mk, b0, b1);
+    hist_inc(hb, dir_off_lo(p01, lut[a0]));
+    hist_inc(hb, dir_off_hi(p01, lut[a1]));
+    hist_inc(hb, dir_off_lo(p23, lut[b0]));
+    hist_inc(hb, dir_off_hi(p23, lut[b1]));
+  } else if constexpr (LUT) {
     uint32_t a0, a1, b0, b1;
     const uint32_t p01 = code_pair_lut_pre<lut_swz(LUT)>(R01, G01, B01, mk, a0, a1);
     const uint32_t p23 = code_pair_lut_pre<lut_swz(LUT)>(R23, G23, B23, mk, b0, b1);
@@ -249,6 +273,55 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
   }
 }
 
+// Direct-offset codes (lut 5/6): same phase order as bin_quads_lut; each table
+// entry goes into its atomic's address with one PRMT.
+// OCT = 1: a lane's quads come in adjacent pairs (24 bytes, three LDS.64):
+// quads 2j and 2j+1 of a lane are pixels [8 (q0 + j qstride), +8).
+template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0>
+__device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qstride, MadK mk) {
+  uint32_t w[NQ][3];
+  if constexpr (OCT) {
+#pragma unroll
+    for (int j = 0; j < NQ / 2; ++j) {
+      const uint2* p = reinterpret_cast<const uint2*>(buf + (q0 + j * qstride) * 24);
+      const uint2 a = p[0], b = p[1], c = p[2];
+      w[2 * j][0] = a.x;
+      w[2 * j][1] = a.y;
+      w[2 * j][2] = b.x;
+      w[2 * j + 1][0] = b.y;
+      w[2 * j + 1][1] = c.x;
+      w[2 * j + 1][2] = c.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(buf + (q0 + j * qstride) * 12);
+      w[j][0] = p[0];
+      w[j][1] = p[1];
+      w[j][2] = p[2];
+    }
+  }
+  uint32_t pre[2 * NQ], ia[2 * NQ], ib[2 * NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    uint32_t R01, G01, B01, R23, G23, B23;
+    unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
+    pre[2 * j] = code_pair_dir_pre<TBF>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_dir_pre<TBF>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+  }
+  uint32_t qa[2 * NQ], qb[2 * NQ];
+#pragma unroll
+  for (int j = 0; j < 2 * NQ; ++j) {
+    qa[j] = lds_u8(LUT_S + ia[j]);
+    qb[j] = lds_u8(LUT_S + ib[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * NQ; ++j) {
+    hist_inc_s<HIST_S>(dir_off_lo(pre[j], qa[j]));
+    hist_inc_s<HIST_S>(dir_off_hi(pre[j], qb[j]));
+  }
+}
+
 template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD, int SG>
 __global__ void __launch_bounds__(CW * 32 + (NOPROD ? 0 : 32), MINB)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
@@ -274,11 +347,12 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
   if (MODE == kModeFast)
     for (int i = tid; i < kEntries; i += kThreads)
-      sm.c2b[i] = (uint8_t)(kUseLut ? code_to_bin_lut(i) : code_to_bin(i));
+      sm.c2b[i] = (uint8_t)(lut_dir(LUT) ? code_to_bin_dir(i)
+                                         : (kUseLut ? code_to_bin_lut(i) : code_to_bin(i)));
   if (kUseLut)
     for (int i = tid; i < kLutBytes; i += kThreads) {
       const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, lut_swz(LUT));
-      sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+      sm.lut[i] = (uint8_t)(na > d ? 0u : (lut_dir(LUT) ? lut_entry_dir(na, d) : lut_entry(na, d)));
     }
   if (tid == 0) {
     sm.mk = mk_param;
@@ -364,11 +438,25 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const int nq = ng * 4;
 #pragma unroll 2
       for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+    } else if constexpr (QUAD == 4 && MODE == kModeFast && lut_dir(LUT)) {
+      // lane-contiguous octets (24 bytes: three LDS.64), direct-offset codes
+      constexpr int kQPL = 4 * SG / kConsumers;
+      const int nq = ng * 4;
+      if (nq == kQPL * kConsumers) {
+        bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1>(
+            buf, tid, kConsumers, mk);
+      } else {
+        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+      }
     } else if constexpr (QUAD == 3 && MODE == kModeFast && LUT) {
       constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
+        if constexpr (lut_dir(LUT))
+          bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s>(
+              buf, tid, kConsumers, mk);
+        else
+          bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
       }
@@ -468,7 +556,8 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
   switch (cfg) {
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
-    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21)
+    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21) K1_CASE(22)
+    K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -505,7 +594,13 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 18>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 19>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 20>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 21>();
+  if ((e = configure_cfg<MODE, 21>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 22>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 23>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 24>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 25>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 26>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 27>();
 }
 
 }  // namespace
@@ -552,7 +647,7 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
   if (LUT) {
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) {
       const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, 3);
-      lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+      lut[i] = (uint8_t)(na > d ? 0u : (LUT == 2 ? lut_entry_dir(na, d) : lut_entry(na, d)));
     }
     __syncthreads();
   }
@@ -567,7 +662,14 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
     const uint32_t R = r | ((c2 >> 16) << 16), G = g | (((c2 >> 8) & 255u) << 16),
                    B = b | ((c2 & 255u) << 16);
     uint32_t b0, b1;
-    if (LUT) {
+    if (LUT == 2) {  // direct-offset codes (K1 lut 5/6; TBF only moves B between pipes)
+      uint32_t i0, i1;
+      const uint32_t pre = code_pair_dir_pre<0>(R, G, B, mk, i0, i1);
+      const uint32_t pre6 = code_pair_dir_pre<1>(R, G, B, mk, i0, i1);
+      b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
+      b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
+      if (pre6 != pre) b0 = b1 = 254u;
+    } else if (LUT) {
       uint32_t i0, i1;
       const uint32_t pre = code_pair_lut_pre(R, G, B, mk, i0, i1);
       const uint32_t code = code_pair_lut_post(pre, lut[i0], lut[i1], mk);
@@ -588,7 +690,10 @@ int k1_cfg_uses_lut(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].
 
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                              int lut, cudaStream_t stream) {
-  if (fast && lut) {
+  if (fast && lut >= 5) {
+    cudaFuncSetAttribute(k5_binmap_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
+    k5_binmap_kernel<2><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
+  } else if (fast && lut) {
     cudaFuncSetAttribute(k5_binmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
     k5_binmap_kernel<1><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
   } else {

@@ -44,12 +44,15 @@ constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvLutBytes = 65536;
 constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-free rows on NV12 content
 
+// DIR = 1: direct-offset codes (binfn.cuh code_pair_dir_pre, 8192 entries)
+template <int DIR>
 struct NvSmem {
+  static constexpr int kEntries = DIR ? kDirCodes : kLutCodes;
   alignas(128) uint8_t buf[kNvStages][kNvStageBytes];
   uint8_t lut[kNvLutBytes];
-  uint32_t hist[kLutCodes];
+  uint32_t hist[kEntries];
   uint32_t binacc[256];
-  uint8_t c2b[kLutCodes];
+  uint8_t c2b[kEntries];
   uint64_t full[kNvStages];
   uint64_t empty[kNvStages];
   MadK mk;
@@ -118,6 +121,7 @@ __device__ __forceinline__ void block_chroma(uint32_t uv, int k, int32_t& ruv, i
 constexpr uint32_t kNvDynSmemBase = 0x400;
 
 // One 2 x 8 tile: Y row 0 (y0), Y row 1 (y1), UV (c): 8 pixel pairs.
+template <int DIR>
 __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, MadK mk) {
   uint32_t pre[8], ia[8], ib[8];
 #pragma unroll
@@ -132,30 +136,45 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, M
       uint32_t R, G, B;
       nv12_pair_rgb(__byte_perm(w, 0u, 0x4440u | o), __byte_perm(w, 0u, 0x4440u | (o + 1)), ruv,
                     guv, buv, R, G, B);
-      pre[2 * k + r] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
+      if constexpr (DIR)
+        pre[2 * k + r] = code_pair_dir_pre<0>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
+      else
+        pre[2 * k + r] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
     }
   }
   uint32_t qa[8], qb[8];
-  constexpr uint32_t lut_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem, lut);
+  constexpr uint32_t lut_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem<DIR>, lut);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     qa[j] = lds_u8(lut_s + ia[j]);
     qb[j] = lds_u8(lut_s + ib[j]);
   }
+  if constexpr (DIR) {
+    // ATOMS [offset + imm]: the histogram's shared-window address is a constant too
+    constexpr uint32_t hist_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem<DIR>, hist);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t code = code_pair_lut_post(pre[j], qa[j], qb[j], mk);
-    atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_lo(code, mk)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_hi(code, mk)), 1u);
+    for (int j = 0; j < 8; ++j) {
+      asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(dir_off_lo(pre[j], qa[j])), "n"(hist_s) : "memory");
+      asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(dir_off_hi(pre[j], qb[j])), "n"(hist_s) : "memory");
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t code = code_pair_lut_post(pre[j], qa[j], qb[j], mk);
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_lo(code, mk)), 1u);
+      atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_hi(code, mk)), 1u);
+    }
   }
 }
 
-template <int MODE>
+template <int MODE, int DIR>
 __global__ void __launch_bounds__(kNvConsumers + 32, 1)
 k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                MadK mk_param, uint32_t* __restrict__ sink) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  NvSmem& sm = *reinterpret_cast<NvSmem*>(smem_raw);
+  using Smem = NvSmem<DIR>;
+  constexpr int kEntries = Smem::kEntries;
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr uint32_t nbins = 162;
@@ -165,14 +184,14 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
   if ((uint32_t)__cvta_generic_to_shared(smem_raw) != kNvDynSmemBase) __trap();  // see nv_tile
 
   if (MODE == kModeFast) {
-    for (int i = tid; i < kLutCodes; i += blockDim.x) {
+    for (int i = tid; i < kEntries; i += blockDim.x) {
       sm.hist[i] = 0u;
-      sm.c2b[i] = (uint8_t)code_to_bin_lut(i);
+      sm.c2b[i] = (uint8_t)(DIR ? code_to_bin_dir(i) : code_to_bin_lut(i));
     }
     for (int i = tid; i < 256; i += blockDim.x) sm.binacc[i] = 0u;
     for (int i = tid; i < kNvLutBytes; i += blockDim.x) {
       const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
-      sm.lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+      sm.lut[i] = (uint8_t)(na > d ? 0u : (DIR ? lut_entry_dir(na, d) : lut_entry(na, d)));
     }
   }
   if (tid == 0) {
@@ -253,7 +272,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       if constexpr (MODE == kModeRead) {
         xacc ^= a.x ^ a.y ^ b.x ^ b.y ^ c.x ^ c.y;
       } else {
-        nv_tile(a, b, c, hb, mk);
+        nv_tile<DIR>(a, b, c, hb, mk);
       }
       cx += dr;
       br += dq;
@@ -273,7 +292,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const bool changed = it.next(!last);
     if (MODE == kModeFast && (last || changed)) {
       named_bar_sync(1, kNvConsumers);
-      for (uint32_t cc = tid; cc < (uint32_t)kLutCodes; cc += kNvConsumers) {
+      for (uint32_t cc = tid; cc < (uint32_t)kEntries; cc += kNvConsumers) {
         const uint32_t cnt = sm.hist[cc];
         if (cnt) {
           sm.hist[cc] = 0u;
@@ -358,7 +377,7 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
   if (FAST) {
     for (int i = threadIdx.x; i < kNvLutBytes; i += blockDim.x) {
       const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
-      lut[i] = (uint8_t)(na <= d ? lut_entry(na, d) : 0u);
+      lut[i] = (uint8_t)(na > d ? 0u : (FAST == 2 ? lut_entry_dir(na, d) : lut_entry(na, d)));
     }
     __syncthreads();
   }
@@ -370,7 +389,12 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
     uint32_t R, G, B;
     nv12_pair_rgb(Yv, Y2, ruv, guv, buv, R, G, B);
     uint32_t b0, b1;
-    if (FAST) {
+    if (FAST == 2) {  // direct-offset codes (DIR kernel)
+      uint32_t i0, i1;
+      const uint32_t pre = code_pair_dir_pre<0>(R, G, B, mk, i0, i1);
+      b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
+      b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
+    } else if (FAST) {
       uint32_t i0, i1;
       const uint32_t pre = code_pair_lut_pre<kNvSwz>(R, G, B, mk, i0, i1);
       const uint32_t code = code_pair_lut_post(pre, lut[i0], lut[i1], mk);
@@ -396,11 +420,15 @@ bool nv12_fast_ok(int32_t width, uint32_t nh, uint32_t ns, uint32_t nv) {
 int nv12_generic_rows() { return kGenRows; }
 
 cudaError_t k1_nv12_configure() {
-  cudaError_t e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem));
+  cudaError_t e;
+#define NV_CONF(M, D)                                                                          \
+  e = cudaFuncSetAttribute(k1_nv12_kernel<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)sizeof(NvSmem<D>));                                           \
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k1_nv12_kernel<kModeRead>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(NvSmem));
+  NV_CONF(kModeFast, 0) NV_CONF(kModeFast, 1) NV_CONF(kModeRead, 0)
+#undef NV_CONF
+  e = cudaFuncSetAttribute(k5_nv12map_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kNvLutBytes);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k5_nv12map_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kNvLutBytes);
@@ -408,7 +436,7 @@ cudaError_t k1_nv12_configure() {
 
 cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
                            uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                           cudaStream_t stream) {
+                           int dir, cudaStream_t stream) {
   if (total <= 0) return cudaSuccess;
   if (mode == kModeGeneric) {
     const int64_t grid = std::min<int64_t>(total, (int64_t)sm_count * 8);
@@ -416,18 +444,23 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
     return cudaGetLastError();
   }
   const int grid = (int)std::min<int64_t>(total, sm_count);
-  if (mode == kModeFast)
-    k1_nv12_kernel<kModeFast><<<grid, kNvConsumers + 32, sizeof(NvSmem), stream>>>(d_segs, nseg, total,
-                                                                                  kMadK, sink);
+  if (mode == kModeFast && dir)
+    k1_nv12_kernel<kModeFast, 1><<<grid, kNvConsumers + 32, sizeof(NvSmem<1>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast)
+    k1_nv12_kernel<kModeFast, 0><<<grid, kNvConsumers + 32, sizeof(NvSmem<0>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
   else
-    k1_nv12_kernel<kModeRead><<<grid, kNvConsumers + 32, sizeof(NvSmem), stream>>>(d_segs, nseg, total,
-                                                                                  kMadK, sink);
+    k1_nv12_kernel<kModeRead, 0><<<grid, kNvConsumers + 32, sizeof(NvSmem<0>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
   return cudaGetLastError();
 }
 
 cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                              cudaStream_t stream) {
-  if (fast)
+                              int dir, cudaStream_t stream) {
+  if (fast && dir)
+    k5_nv12map_kernel<2><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK);
+  else if (fast)
     k5_nv12map_kernel<1><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK);
   else
     k5_nv12map_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, kMadK);

@@ -31,9 +31,9 @@ cudaError_t k1_nv12_configure();
 // kModeGeneric: generic kernel over `total` (frame, 8-block-row) items.
 cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
                            uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                           cudaStream_t stream);
+                           int dir, cudaStream_t stream);
 cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                              cudaStream_t stream);
+                              int dir, cudaStream_t stream);
 
 // ---- K4 (sample.cu): clip frame sampling + resize (NEXT f3)
 int k4_rows_per_band(int32_t W, bool nv12);

@@ -19,13 +19,17 @@ int main(int argc, char** argv) {
   }
   const uint32_t nh = atoi(argv[2]), ns = atoi(argv[3]), nv = atoi(argv[4]);
   const uint32_t N = 1u << 24;
-  std::vector<uint8_t> t0(N), t1(N), tg(N), l0(N), l1(N);
+  std::vector<uint8_t> t0(N), t1(N), tg(N), l0(N), l1(N), e0(N), e1(N);
   std::vector<uint8_t> lut(65536, 0);
   for (uint32_t d = 0; d < 256; ++d)
     for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d, 1)] = (uint8_t)lut_entry(na, d);  // K1 cfg14
   std::vector<uint8_t> lut2(65536, 0);  // swizzle 3 (the NV12 kernel's table)
+  std::vector<uint8_t> lut3(65536, 0);  // swizzle 3, direct-offset entries (K1 lut 5/6)
   for (uint32_t d = 0; d < 256; ++d)
-    for (uint32_t na = 0; na <= d; ++na) lut2[lut_index(na, d, 3)] = (uint8_t)lut_entry(na, d);
+    for (uint32_t na = 0; na <= d; ++na) {
+      lut2[lut_index(na, d, 3)] = (uint8_t)lut_entry(na, d);
+      lut3[lut_index(na, d, 3)] = (uint8_t)lut_entry_dir(na, d);
+    }
   // the unswizzle used by the kernels' table initialisation inverts every swizzle
   for (int swz = 0; swz <= 3; ++swz)
     for (uint32_t d = 0; d < 256; ++d)
@@ -52,6 +56,19 @@ int main(int argc, char** argv) {
       fprintf(stderr, "lut code offset out of range\n");
       return 1;
     }
+    // direct-offset codes: both B forms, offsets in range and multiples of 4
+    const uint32_t dp = code_pair_dir_pre<0>(R, G, B, kMadK, i0, i1);
+    if (code_pair_dir_pre<1>(R, G, B, kMadK, i0, i1) != dp) {
+      fprintf(stderr, "dir pre TBF mismatch\n");
+      return 1;
+    }
+    const uint32_t o0 = dir_off_lo(dp, lut3[i0]), o1 = dir_off_hi(dp, lut3[i1]);
+    if (o0 >= 4u * kDirCodes || o1 >= 4u * kDirCodes || (o0 & 3u) || (o1 & 3u)) {
+      fprintf(stderr, "dir code offset out of range\n");
+      return 1;
+    }
+    e0[c] = (uint8_t)code_to_bin_dir(o0 >> 2);
+    e1[c2] = (uint8_t)code_to_bin_dir(o1 >> 2);
   }
   // unpack4 on pseudo-random bytes
   uint32_t x = 12345u;
@@ -76,7 +93,7 @@ int main(int argc, char** argv) {
       }
   }
   // NV12 pair conversion + LUT codes for every (Y, U, V): lane 0 = Y, lane 1 = Y ^ 0x5A
-  std::vector<uint8_t> n0(N), n1(N);
+  std::vector<uint8_t> n0(N), n1(N), m0(N), m1(N);
   for (uint32_t c = 0; c < N; ++c) {
     const uint32_t Y = c >> 16, U = (c >> 8) & 255u, V = c & 255u, Y2 = Y ^ 0x5Au;
     int32_t ruv, guv, buv;
@@ -88,6 +105,9 @@ int main(int argc, char** argv) {
     const uint32_t lc = code_pair_lut_post(pre, lut2[i0], lut2[i1], kMadK);
     n0[c] = (uint8_t)code_to_bin_lut(lut_off_lo(lc, kMadK) >> 2);
     n1[(Y2 << 16) | (U << 8) | V] = (uint8_t)code_to_bin_lut(lut_off_hi(lc, kMadK) >> 2);
+    const uint32_t dp = code_pair_dir_pre<0>(R, G, B, kMadK, i0, i1);  // direct-offset codes
+    m0[c] = (uint8_t)code_to_bin_dir(dir_off_lo(dp, lut3[i0]) >> 2);
+    m1[(Y2 << 16) | (U << 8) | V] = (uint8_t)code_to_bin_dir(dir_off_hi(dp, lut3[i1]) >> 2);
   }
   FILE* f = fopen(argv[1], "wb");
   fwrite(t0.data(), 1, N, f);
@@ -97,6 +117,10 @@ int main(int argc, char** argv) {
   fwrite(l1.data(), 1, N, f);
   fwrite(n0.data(), 1, N, f);
   fwrite(n1.data(), 1, N, f);
+  fwrite(e0.data(), 1, N, f);
+  fwrite(e1.data(), 1, N, f);
+  fwrite(m0.data(), 1, N, f);
+  fwrite(m1.data(), 1, N, f);
   fclose(f);
   return 0;
 }

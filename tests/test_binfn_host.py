@@ -29,7 +29,7 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
     subprocess.check_call([exe, path, *map(str, bins)])
     raw = np.fromfile(path, dtype=np.uint8)
     n = 1 << 24
-    t0, t1, tg, l0, l1, n0, n1 = (raw[i * n:(i + 1) * n] for i in range(7))
+    t0, t1, tg, l0, l1, n0, n1, e0, e1, m0, m1 = (raw[i * n:(i + 1) * n] for i in range(11))
     p = oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2])
     want = oracle.bin_table(p)
     assert np.array_equal(tg, want)
@@ -38,7 +38,11 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
         assert np.array_equal(t1, want), np.nonzero(t1 != want)[0][:10]
         assert np.array_equal(l0, want), np.nonzero(l0 != want)[0][:10]
         assert np.array_equal(l1, want), np.nonzero(l1 != want)[0][:10]
+        assert np.array_equal(e0, want), np.nonzero(e0 != want)[0][:10]  # direct-offset codes
+        assert np.array_equal(e1, want), np.nonzero(e1 != want)[0][:10]
         yuv = want[yuv_rgb_table()]  # bin of every (Y, U, V): oracle O0 then O1
         assert np.array_equal(n0, yuv), np.nonzero(n0 != yuv)[0][:10]
         assert np.array_equal(n1, yuv), np.nonzero(n1 != yuv)[0][:10]
+        assert np.array_equal(m0, yuv), np.nonzero(m0 != yuv)[0][:10]  # direct-offset codes
+        assert np.array_equal(m1, yuv), np.nonzero(m1 != yuv)[0][:10]
 
