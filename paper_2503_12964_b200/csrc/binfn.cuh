@@ -112,10 +112,10 @@ struct MadK {
   uint32_t sl4;   // 2^4
   uint32_t sl16;  // 2^16
   uint32_t sl20;  // 2^20
-  uint32_t four, neg4, neg6;
+  uint32_t four, neg4, neg6, neg7;
 };
 constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20,
-                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu};
+                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu, 0xFFFFFFF9u};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -273,16 +273,38 @@ CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
 // Each lane's code IS the byte offset of its code-histogram entry, so nothing
 // runs between the table lookup and the shared-memory atomic but one PRMT:
 //   offset = byte1 << 8 | byte0,
-//   byte0 = the table entry (qr | qf << 2) << 2   (bits 2-5; bits 0-1, 6-7 zero),
+//   byte0 = the table entry: q3 << 2 | hash << 5  (bits 0-1 zero),
 //   byte1 = v (bits 8-9) | s1 (10) | s2 (11) | A = [r>=g] (12) | B = [g>=b] (13)
 //           | C = [r>=b] (14) | 0 (15)          -> offsets < 0x8000: 8192 entries.
+// q3 in [0, 8) is the compact index of the table's (qr, qf) pair (kDirQ below);
+// hash (2 bits, a function of (d, na) that the bin ignores) only spreads the
+// entries over the 32 shared-memory banks: the bank of an entry is offset bits
+// 2-6 = (q3, hash), all from byte 0.  Without it a warp's atomics on noisy
+// content would share 8 banks.
 // The byte-1 fields are threshold bits (a - b + 2^j, see code_pair) merged by
 // bit-selects: every select takes ONE field from its source and keeps the rest,
 // and the field values never carry into bit 15.  The table index is the
 // swizzle-3 index (na + 4d) mod 256, computed straight from the channel sum:
 //   na + 4d = (r + g + b) + 3 max - 6 min   (mid = sum - max - min).
 constexpr int kDirCodes = 8192;
-CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d) { return lut_entry(na, d) << 2; }
+// (qr, qf) of q3 = 0..7: grey, then na/d = 0, (0,1/3), 1/3, (1/3,2/3), 2/3, (2/3,1), 1
+constexpr uint32_t kDirQ = (0u << 0) | (12u << 4) | (8u << 8) | (9u << 12) | (5u << 16) |
+                           (6u << 20) | (2u << 24) | (3u << 28);  // nibble = qr | qf << 2
+CD_HD uint32_t dir_q3(uint32_t q) {  // (qr | qf << 2) -> q3
+  for (uint32_t i = 0; i < 8; ++i)
+    if (((kDirQ >> (4 * i)) & 15u) == q) return i;
+  return 0u;
+}
+// hash modes: 0 none, 1 d & 3, 2 na & 3, 3 (d ^ na) & 3, 4 ((d >> 5) ^ na) & 3,
+// 5 ((d >> 6) ^ d) & 3
+CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d, int hash = 1) {
+  const uint32_t h = hash == 1 ? d
+                     : hash == 2 ? na
+                     : hash == 3 ? (d ^ na)
+                     : hash == 4 ? ((d >> 5) ^ na)
+                     : hash == 5 ? ((d >> 6) ^ d) : 0u;
+  return (dir_q3(lut_entry(na, d)) << 2) | ((h & 3u) << 5);
+}
 
 // bit select (a where m, else b) as ONE LOP3: written as inline PTX so that the
 // compiler does not flatten a chain of selects into and-or terms (one more op)
@@ -297,17 +319,23 @@ CD_HD uint32_t cd_sel(uint32_t a, uint32_t b) {
 #endif
 }
 
+// Table index with swizzle multiplier KS: byte (na + KS d) mod 256 of row d.
+CD_HD uint32_t lut_index_k(uint32_t na, uint32_t d, uint32_t ks) { return d * 256u + ((na + ks * d) & 255u); }
+CD_HD uint32_t lut_unswizzle_k(uint32_t b, uint32_t d, uint32_t ks) { return (b - ks * d) & 255u; }
+
 // Part 1: byte 1 of both lanes' offsets (in bytes 1 and 3 of the result) and
 // the two table indices.  TBF = 1 computes B on the FMA pipe (two IMADs)
-// instead of one IADD3 on the ALU pipe.
-template <int TBF = 0>
+// instead of one IADD3 on the ALU pipe.  KS = table swizzle multiplier (4 or 5):
+// na + KS d = sum + (KS - 1) max - (KS + 2) min.
+template <int TBF = 0, int KS = 4>
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
+  static_assert(KS == 4 || KS == 5, "swizzle multiplier");
   const uint32_t mx = cd_max3_u16x2(R, G, B);
   const uint32_t mn = cd_min3_u16x2(R, G, B);
   const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, k.three, R)));
-  const uint32_t nas = cd_mad(mn, k.neg6, t);  // na + 4d; lanes in [0, 1275]
+  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, KS == 4 ? k.three : k.four, R)));
+  const uint32_t nas = cd_mad(mn, KS == 4 ? k.neg6 : k.neg7, t);  // na + KS d; lanes < 2^16
   i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8
   i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
   const uint32_t tA = R + 0x10001000u - G;  // bit 12: r >= g   (IADD3)
@@ -331,7 +359,8 @@ CD_HD uint32_t dir_off_hi(uint32_t pre, uint32_t q1) { return cd_prmt(q1, pre, 0
 // code index (byte offset / 4) -> bin in [0,162), or 255 for an unreachable code.
 CD_HD uint32_t code_to_bin_dir(uint32_t idx) {
   const uint32_t c = idx << 2;
-  const uint32_t qr = (c >> 2) & 3u, qf = (c >> 4) & 3u, z = (c >> 6) & 3u, v = (c >> 8) & 3u;
+  const uint32_t q = (kDirQ >> (4 * ((c >> 2) & 7u))) & 15u;
+  const uint32_t qr = q & 3u, qf = q >> 2, z = (c >> 7) & 1u, v = (c >> 8) & 3u;
   const uint32_t s1 = (c >> 10) & 1u, s2 = (c >> 11) & 1u, A = (c >> 12) & 1u;
   const uint32_t B = (c >> 13) & 1u, C = (c >> 14) & 1u, z2 = c >> 15;
   const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector

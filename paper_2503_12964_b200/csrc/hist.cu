@@ -55,15 +55,29 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {4, 1, 16, 5, 3}, {4, 1, 16, 6, 3},  // lut 5/6 = direct offsets
                            {4, 1, 16, 5, 4},   // quad 4 = lane-contiguous octets (LDS.64)
                            {4, 1, 8, 5, 3}, {3, 1, 16, 5, 3, 0, 768},  // fewer ring hand-offs per pixel
-                           {3, 1, 16, 5, 4, 0, 768}};
-constexpr int kNumCfgs = 28;
+                           {3, 1, 16, 5, 4, 0, 768},
+                           {4, 1, 16, 7, 3}, {4, 1, 16, 8, 3}, {4, 1, 16, 9, 3},  // bank hashes
+                           {4, 1, 16, 8, 4}, {4, 1, 16, 10, 3}, {4, 1, 16, 11, 3}, {4, 1, 16, 10, 4},
+                           {4, 1, 16, 12, 3}, {4, 1, 16, 12, 4},  // lut 12: swizzle multiplier 5
+                           {3, 1, 24, 10, 3, 0, 768}, {4, 1, 20, 10, 3, 0, 640},  // more warps
+                           {3, 1, 24, 12, 3, 0, 768}, {4, 1, 20, 12, 3, 0, 640},
+                           {4, 1, 32, 10, 3, 1}, {2, 1, 32, 10, 3, 1, 1024}};  // 32 warps, no producer
+constexpr int kNumCfgs = 43;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
   return lut == 1 ? 1 : (lut == 3 ? 2 : (lut >= 4 ? 3 : 0));
 }
-// lut 5 / 6: direct-offset codes (binfn.cuh code_pair_dir_pre; 6 = B on the FMA pipe)
+// lut 5-9: direct-offset codes (binfn.cuh code_pair_dir_pre; 6 = B on the FMA pipe),
+// bank hash of the table entries (binfn.cuh lut_entry_dir): 7 none, 8 na & 3,
+// 9 (d ^ na) & 3, 10 and 12 ((d >> 5) ^ na) & 3, 11 ((d >> 6) ^ d) & 3, otherwise d & 3
+// (tools/atoms_bank_sim.py)
 __host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
+__host__ __device__ constexpr int lut_hash(int lut) {
+  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
+}
+// table swizzle multiplier of the direct-offset configs: lut 12 = 5, else 4
+__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 ? 5 : 4; }
 
 template <int STAGES, int LUT, int SG>
 struct K1Smem {
@@ -211,8 +225,8 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
   if constexpr (lut_dir(LUT)) {
     uint32_t a0, a1, b0, b1;
-    const uint32_t p01 = code_pair_dir_pre<LUT == 6>(R01, G01, B01, mk, a0, a1);
-    const uint32_t p23 = code_pair_dir_pre<LUT == 6>(R23, G23, B23, mk, b0, b1);
+    const uint32_t p01 = code_pair_dir_pre<LUT == 6, lut_ks(LUT)>(R01, G01, B01, mk, a0, a1);
+    const uint32_t p23 = code_pair_dir_pre<LUT == 6, lut_ks(LUT)>(R23, G23, B23, mk, b0, b1);
     hist_inc(hb, dir_off_lo(p01, lut[a0]));
     hist_inc(hb, dir_off_hi(p01, lut[a1]));
     hist_inc(hb, dir_off_lo(p23, lut[b0]));
@@ -277,7 +291,7 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
 // entry goes into its atomic's address with one PRMT.
 // OCT = 1: a lane's quads come in adjacent pairs (24 bytes, three LDS.64):
 // quads 2j and 2j+1 of a lane are pixels [8 (q0 + j qstride), +8).
-template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0>
+template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0, int KS = 4>
 __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qstride, MadK mk) {
   uint32_t w[NQ][3];
   if constexpr (OCT) {
@@ -306,8 +320,8 @@ __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qs
   for (int j = 0; j < NQ; ++j) {
     uint32_t R01, G01, B01, R23, G23, B23;
     unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
-    pre[2 * j] = code_pair_dir_pre<TBF>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-    pre[2 * j + 1] = code_pair_dir_pre<TBF>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    pre[2 * j] = code_pair_dir_pre<TBF, KS>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_dir_pre<TBF, KS>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
   }
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
@@ -351,8 +365,11 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
                                          : (kUseLut ? code_to_bin_lut(i) : code_to_bin(i)));
   if (kUseLut)
     for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, lut_swz(LUT));
-      sm.lut[i] = (uint8_t)(na > d ? 0u : (lut_dir(LUT) ? lut_entry_dir(na, d) : lut_entry(na, d)));
+      const uint32_t d = (uint32_t)i >> 8,
+                     na = lut_dir(LUT) ? lut_unswizzle_k((uint32_t)i & 255u, d, lut_ks(LUT))
+                                       : lut_unswizzle((uint32_t)i & 255u, d, lut_swz(LUT));
+      sm.lut[i] = (uint8_t)(na > d ? 0u
+                                   : (lut_dir(LUT) ? lut_entry_dir(na, d, lut_hash(LUT)) : lut_entry(na, d)));
     }
   if (tid == 0) {
     sm.mk = mk_param;
@@ -443,7 +460,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1>(
+        bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1, lut_ks(LUT)>(
             buf, tid, kConsumers, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
@@ -453,7 +470,8 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
         if constexpr (lut_dir(LUT))
-          bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s>(
+          bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 0,
+                        lut_ks(LUT)>(
               buf, tid, kConsumers, mk);
         else
           bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
@@ -557,7 +575,9 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
     K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
     K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
     K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21) K1_CASE(22)
-    K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27)
+    K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27) K1_CASE(28) K1_CASE(29)
+    K1_CASE(30) K1_CASE(31) K1_CASE(32) K1_CASE(33) K1_CASE(34) K1_CASE(35) K1_CASE(36)
+    K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -600,7 +620,22 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 24>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 25>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 26>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 27>();
+  if ((e = configure_cfg<MODE, 27>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 28>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 29>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 30>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 31>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 32>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 33>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 34>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 35>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 36>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 37>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 38>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 39>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 40>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 41>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 42>();
 }
 
 }  // namespace
@@ -642,12 +677,12 @@ namespace {
 template <int LUT>
 __global__ void __launch_bounds__(256)
 k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                 MadK mk) {
+                 MadK mk, int hash, int ks) {
   extern __shared__ __align__(16) uint8_t lut[];
   if (LUT) {
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, 3);
-      lut[i] = (uint8_t)(na > d ? 0u : (LUT == 2 ? lut_entry_dir(na, d) : lut_entry(na, d)));
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle_k((uint32_t)i & 255u, d, (uint32_t)ks);
+      lut[i] = (uint8_t)(na > d ? 0u : (LUT == 2 ? lut_entry_dir(na, d, hash) : lut_entry(na, d)));
     }
     __syncthreads();
   }
@@ -664,11 +699,14 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
     uint32_t b0, b1;
     if (LUT == 2) {  // direct-offset codes (K1 lut 5/6; TBF only moves B between pipes)
       uint32_t i0, i1;
-      const uint32_t pre = code_pair_dir_pre<0>(R, G, B, mk, i0, i1);
-      const uint32_t pre6 = code_pair_dir_pre<1>(R, G, B, mk, i0, i1);
+      const uint32_t pre = ks == 5 ? code_pair_dir_pre<0, 5>(R, G, B, mk, i0, i1)
+                                   : code_pair_dir_pre<0, 4>(R, G, B, mk, i0, i1);
+      uint32_t j0, j1;
+      const uint32_t pre6 = ks == 5 ? code_pair_dir_pre<1, 5>(R, G, B, mk, j0, j1)
+                                    : code_pair_dir_pre<1, 4>(R, G, B, mk, j0, j1);
       b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
       b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
-      if (pre6 != pre) b0 = b1 = 254u;
+      if (pre6 != pre || j0 != i0 || j1 != i1) b0 = b1 = 254u;
     } else if (LUT) {
       uint32_t i0, i1;
       const uint32_t pre = code_pair_lut_pre(R, G, B, mk, i0, i1);
@@ -692,12 +730,13 @@ cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv
                              int lut, cudaStream_t stream) {
   if (fast && lut >= 5) {
     cudaFuncSetAttribute(k5_binmap_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
-    k5_binmap_kernel<2><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
+    k5_binmap_kernel<2><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK, lut_hash(lut),
+                                                             lut_ks(lut));
   } else if (fast && lut) {
     cudaFuncSetAttribute(k5_binmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
-    k5_binmap_kernel<1><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
+    k5_binmap_kernel<1><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK, 0, 4);
   } else {
-    k5_binmap_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, fast, kMadK);
+    k5_binmap_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, fast, kMadK, 0, 4);
   }
   return cudaGetLastError();
 }

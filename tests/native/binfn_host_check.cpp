@@ -24,11 +24,13 @@ int main(int argc, char** argv) {
   for (uint32_t d = 0; d < 256; ++d)
     for (uint32_t na = 0; na <= d; ++na) lut[lut_index(na, d, 1)] = (uint8_t)lut_entry(na, d);  // K1 cfg14
   std::vector<uint8_t> lut2(65536, 0);  // swizzle 3 (the NV12 kernel's table)
-  std::vector<uint8_t> lut3(65536, 0);  // swizzle 3, direct-offset entries (K1 lut 5/6)
+  std::vector<uint8_t> lut3(65536, 0);  // swizzle 3, direct-offset entries, d & 3 bank hash
+  std::vector<uint8_t> lut4(65536, 0);  // swizzle multiplier 5, ((d >> 5) ^ na) & 3 bank hash
   for (uint32_t d = 0; d < 256; ++d)
     for (uint32_t na = 0; na <= d; ++na) {
       lut2[lut_index(na, d, 3)] = (uint8_t)lut_entry(na, d);
-      lut3[lut_index(na, d, 3)] = (uint8_t)lut_entry_dir(na, d);
+      lut3[lut_index(na, d, 3)] = (uint8_t)lut_entry_dir(na, d, 1);
+      lut4[lut_index_k(na, d, 5)] = (uint8_t)lut_entry_dir(na, d, 4);
     }
   // the unswizzle used by the kernels' table initialisation inverts every swizzle
   for (int swz = 0; swz <= 3; ++swz)
@@ -62,7 +64,12 @@ int main(int argc, char** argv) {
       fprintf(stderr, "dir pre TBF mismatch\n");
       return 1;
     }
-    const uint32_t o0 = dir_off_lo(dp, lut3[i0]), o1 = dir_off_hi(dp, lut3[i1]);
+    // odd colours: swizzle multiplier 5 and another bank hash (the bin must not depend on either)
+    uint32_t k0 = i0, k1 = i1;
+    const uint32_t dp5 = code_pair_dir_pre<0, 5>(R, G, B, kMadK, k0, k1);
+    const bool odd = c & 1u;
+    const uint32_t o0 = odd ? dir_off_lo(dp5, lut4[k0]) : dir_off_lo(dp, lut3[i0]);
+    const uint32_t o1 = odd ? dir_off_hi(dp5, lut4[k1]) : dir_off_hi(dp, lut3[i1]);
     if (o0 >= 4u * kDirCodes || o1 >= 4u * kDirCodes || (o0 & 3u) || (o1 & 3u)) {
       fprintf(stderr, "dir code offset out of range\n");
       return 1;
