@@ -37,7 +37,7 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
-  int nv12_dir = 1;  // K1-NV12 code layout: 1 = direct offsets, 0 = LUT codes (CLIPDETECT_NV12_DIR)
+  int nv12_dir = 1;  // K1-NV12 code layout: 0 = LUT codes, 1-3 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
   int k1_cfg = 14;  // K1 launch configuration: LUT hue, staged lane-contiguous quads, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
@@ -453,7 +453,10 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
     const int c = atoi(e);
     if (c >= 0 && c < k1_num_cfgs()) ctx->k1_cfg = c;
   }
-  if (const char* e = getenv("CLIPDETECT_NV12_DIR")) ctx->nv12_dir = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("CLIPDETECT_NV12_DIR")) {
+    const int c = atoi(e);
+    if (c >= 0 && c <= 3) ctx->nv12_dir = c;
+  }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       k1_nv12_configure() != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {

@@ -324,8 +324,8 @@ CD_HD uint32_t lut_index_k(uint32_t na, uint32_t d, uint32_t ks) { return d * 25
 CD_HD uint32_t lut_unswizzle_k(uint32_t b, uint32_t d, uint32_t ks) { return (b - ks * d) & 255u; }
 
 // Part 1: byte 1 of both lanes' offsets (in bytes 1 and 3 of the result) and
-// the two table indices.  TBF = 1 computes B on the FMA pipe (two IMADs)
-// instead of one IADD3 on the ALU pipe.  KS = table swizzle multiplier (4 or 5):
+// the two table indices.  TBF = 1 computes B (2: A and B) on the FMA pipe (two
+// IMADs each) instead of one IADD3 each on the ALU pipe.  KS = table swizzle multiplier (4 or 5):
 // na + KS d = sum + (KS - 1) max - (KS + 2) min.
 template <int TBF = 0, int KS = 4>
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
@@ -338,7 +338,8 @@ CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t nas = cd_mad(mn, KS == 4 ? k.neg6 : k.neg7, t);  // na + KS d; lanes < 2^16
   i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8
   i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
-  const uint32_t tA = R + 0x10001000u - G;  // bit 12: r >= g   (IADD3)
+  const uint32_t tA = TBF >= 2 ? cd_mad(G, k.neg1, cd_mad(R, k.one, 0x10001000u))
+                                : R + 0x10001000u - G;                 // bit 12: r >= g
   const uint32_t tB = TBF ? cd_mad(B, k.neg1, cd_mad(G, k.one, 0x20002000u))
                           : G + 0x20002000u - B;                       // bit 13: g >= b
   const uint32_t tC = cd_mad(B, k.neg4, cd_mad(R, k.four, 0x40004000u));  // bit 14: r >= b

@@ -61,8 +61,10 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {4, 1, 16, 12, 3}, {4, 1, 16, 12, 4},  // lut 12: swizzle multiplier 5
                            {3, 1, 24, 10, 3, 0, 768}, {4, 1, 20, 10, 3, 0, 640},  // more warps
                            {3, 1, 24, 12, 3, 0, 768}, {4, 1, 20, 12, 3, 0, 640},
-                           {4, 1, 32, 10, 3, 1}, {2, 1, 32, 10, 3, 1, 1024}};  // 32 warps, no producer
-constexpr int kNumCfgs = 43;
+                           {4, 1, 32, 10, 3, 1}, {2, 1, 32, 10, 3, 1, 1024},  // 32 warps, no producer
+                           {4, 1, 16, 13, 3}, {4, 1, 16, 14, 3},  // lut 13/14: A, B on the FMA pipe
+                           {2, 1, 16, 10, 3, 0, 1024}, {2, 1, 32, 14, 3, 1, 1024}};
+constexpr int kNumCfgs = 47;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
@@ -76,8 +78,10 @@ __host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
 __host__ __device__ constexpr int lut_hash(int lut) {
   return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
 }
-// table swizzle multiplier of the direct-offset configs: lut 12 = 5, else 4
-__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 ? 5 : 4; }
+// table swizzle multiplier of the direct-offset configs: lut 12, 14 = 5, else 4
+__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 || lut == 14 ? 5 : 4; }
+// flags A, B on the FMA pipe (code_pair_dir_pre TBF): lut 6 -> B, lut 13, 14 -> A and B
+__host__ __device__ constexpr int lut_tbf(int lut) { return lut == 6 ? 1 : (lut == 13 || lut == 14 ? 2 : 0); }
 
 template <int STAGES, int LUT, int SG>
 struct K1Smem {
@@ -225,8 +229,8 @@ __device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, con
   unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
   if constexpr (lut_dir(LUT)) {
     uint32_t a0, a1, b0, b1;
-    const uint32_t p01 = code_pair_dir_pre<LUT == 6, lut_ks(LUT)>(R01, G01, B01, mk, a0, a1);
-    const uint32_t p23 = code_pair_dir_pre<LUT == 6, lut_ks(LUT)>(R23, G23, B23, mk, b0, b1);
+    const uint32_t p01 = code_pair_dir_pre<lut_tbf(LUT), lut_ks(LUT)>(R01, G01, B01, mk, a0, a1);
+    const uint32_t p23 = code_pair_dir_pre<lut_tbf(LUT), lut_ks(LUT)>(R23, G23, B23, mk, b0, b1);
     hist_inc(hb, dir_off_lo(p01, lut[a0]));
     hist_inc(hb, dir_off_hi(p01, lut[a1]));
     hist_inc(hb, dir_off_lo(p23, lut[b0]));
@@ -326,8 +330,14 @@ __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qs
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
+#ifdef CLIPDETECT_EXP_NO_TABLE
+    // experiment build only (tools/): a table-free stand-in entry (wrong bins)
+    qa[j] = ia[j] & 0x7Cu;
+    qb[j] = ib[j] & 0x7Cu;
+#else
     qa[j] = lds_u8(LUT_S + ia[j]);
     qb[j] = lds_u8(LUT_S + ib[j]);
+#endif
   }
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
@@ -460,7 +470,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1, lut_ks(LUT)>(
+        bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1, lut_ks(LUT)>(
             buf, tid, kConsumers, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
@@ -470,7 +480,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
         if constexpr (lut_dir(LUT))
-          bin_quads_dir<kQPL, LUT == 6, kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 0,
+          bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 0,
                         lut_ks(LUT)>(
               buf, tid, kConsumers, mk);
         else
@@ -577,7 +587,8 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
     K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21) K1_CASE(22)
     K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27) K1_CASE(28) K1_CASE(29)
     K1_CASE(30) K1_CASE(31) K1_CASE(32) K1_CASE(33) K1_CASE(34) K1_CASE(35) K1_CASE(36)
-    K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42)
+    K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42) K1_CASE(43)
+    K1_CASE(44) K1_CASE(45) K1_CASE(46)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -635,7 +646,11 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 39>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 40>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 41>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 42>();
+  if ((e = configure_cfg<MODE, 42>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 43>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 44>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 45>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 46>();
 }
 
 }  // namespace
@@ -704,9 +719,12 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
       uint32_t j0, j1;
       const uint32_t pre6 = ks == 5 ? code_pair_dir_pre<1, 5>(R, G, B, mk, j0, j1)
                                     : code_pair_dir_pre<1, 4>(R, G, B, mk, j0, j1);
+      const uint32_t pre13 = ks == 5 ? code_pair_dir_pre<2, 5>(R, G, B, mk, j0, j1)
+                                     : code_pair_dir_pre<2, 4>(R, G, B, mk, j0, j1);
+      if (pre13 != pre) b0 = b1 = 253u;
       b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
       b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
-      if (pre6 != pre || j0 != i0 || j1 != i1) b0 = b1 = 254u;
+      if (pre6 != pre || pre13 != pre || j0 != i0 || j1 != i1) b0 = b1 = 254u;
     } else if (LUT) {
       uint32_t i0, i1;
       const uint32_t pre = code_pair_lut_pre(R, G, B, mk, i0, i1);

@@ -44,7 +44,11 @@ constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvLutBytes = 65536;
 constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-free rows on NV12 content
 
-// DIR = 1: direct-offset codes (binfn.cuh code_pair_dir_pre, 8192 entries)
+// DIR > 0: direct-offset codes (binfn.cuh code_pair_dir_pre, 8192 entries):
+// 1 = bank hash d & 3, table swizzle multiplier 4; 2 = hash ((d >> 5) ^ na) & 3,
+// multiplier 4; 3 = that hash, multiplier 5 (CLIPDETECT_NV12_DIR selects)
+__host__ __device__ constexpr int nv_hash(int dir) { return dir == 1 ? 1 : 4; }
+__host__ __device__ constexpr int nv_ks(int dir) { return dir == 3 ? 5 : 4; }
 template <int DIR>
 struct NvSmem {
   static constexpr int kEntries = DIR ? kDirCodes : kLutCodes;
@@ -137,7 +141,7 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, M
       nv12_pair_rgb(__byte_perm(w, 0u, 0x4440u | o), __byte_perm(w, 0u, 0x4440u | (o + 1)), ruv,
                     guv, buv, R, G, B);
       if constexpr (DIR)
-        pre[2 * k + r] = code_pair_dir_pre<0>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
+        pre[2 * k + r] = code_pair_dir_pre<0, nv_ks(DIR)>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
       else
         pre[2 * k + r] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
     }
@@ -190,8 +194,10 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     }
     for (int i = tid; i < 256; i += blockDim.x) sm.binacc[i] = 0u;
     for (int i = tid; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
-      sm.lut[i] = (uint8_t)(na > d ? 0u : (DIR ? lut_entry_dir(na, d) : lut_entry(na, d)));
+      const uint32_t d = (uint32_t)i >> 8,
+                     na = DIR ? lut_unswizzle_k((uint32_t)i & 255u, d, nv_ks(DIR))
+                              : lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
+      sm.lut[i] = (uint8_t)(na > d ? 0u : (DIR ? lut_entry_dir(na, d, nv_hash(DIR)) : lut_entry(na, d)));
     }
   }
   if (tid == 0) {
@@ -372,12 +378,15 @@ k1_nv12_generic_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t t
 // 0 result, out[1][...] = lane 1 result.
 template <int FAST>
 __global__ void __launch_bounds__(256)
-k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, MadK mk) {
+k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, MadK mk,
+                  int dir) {
   extern __shared__ __align__(16) uint8_t lut[];
   if (FAST) {
     for (int i = threadIdx.x; i < kNvLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
-      lut[i] = (uint8_t)(na > d ? 0u : (FAST == 2 ? lut_entry_dir(na, d) : lut_entry(na, d)));
+      const uint32_t d = (uint32_t)i >> 8,
+                     na = FAST == 2 ? lut_unswizzle_k((uint32_t)i & 255u, d, nv_ks(dir))
+                                    : lut_unswizzle((uint32_t)i & 255u, d, kNvSwz);
+      lut[i] = (uint8_t)(na > d ? 0u : (FAST == 2 ? lut_entry_dir(na, d, nv_hash(dir)) : lut_entry(na, d)));
     }
     __syncthreads();
   }
@@ -391,7 +400,8 @@ k5_nv12map_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t 
     uint32_t b0, b1;
     if (FAST == 2) {  // direct-offset codes (DIR kernel)
       uint32_t i0, i1;
-      const uint32_t pre = code_pair_dir_pre<0>(R, G, B, mk, i0, i1);
+      const uint32_t pre = nv_ks(dir) == 5 ? code_pair_dir_pre<0, 5>(R, G, B, mk, i0, i1)
+                                           : code_pair_dir_pre<0, 4>(R, G, B, mk, i0, i1);
       b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
       b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
     } else if (FAST) {
@@ -425,7 +435,8 @@ cudaError_t k1_nv12_configure() {
   e = cudaFuncSetAttribute(k1_nv12_kernel<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)sizeof(NvSmem<D>));                                           \
   if (e != cudaSuccess) return e;
-  NV_CONF(kModeFast, 0) NV_CONF(kModeFast, 1) NV_CONF(kModeRead, 0)
+  NV_CONF(kModeFast, 0) NV_CONF(kModeFast, 1) NV_CONF(kModeFast, 2) NV_CONF(kModeFast, 3)
+  NV_CONF(kModeRead, 0)
 #undef NV_CONF
   e = cudaFuncSetAttribute(k5_nv12map_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kNvLutBytes);
@@ -444,8 +455,14 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
     return cudaGetLastError();
   }
   const int grid = (int)std::min<int64_t>(total, sm_count);
-  if (mode == kModeFast && dir)
+  if (mode == kModeFast && dir == 1)
     k1_nv12_kernel<kModeFast, 1><<<grid, kNvConsumers + 32, sizeof(NvSmem<1>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 2)
+    k1_nv12_kernel<kModeFast, 2><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 3)
+    k1_nv12_kernel<kModeFast, 3><<<grid, kNvConsumers + 32, sizeof(NvSmem<3>), stream>>>(
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast)
     k1_nv12_kernel<kModeFast, 0><<<grid, kNvConsumers + 32, sizeof(NvSmem<0>), stream>>>(
@@ -459,11 +476,11 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
 cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                               int dir, cudaStream_t stream) {
   if (fast && dir)
-    k5_nv12map_kernel<2><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK);
+    k5_nv12map_kernel<2><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK, dir);
   else if (fast)
-    k5_nv12map_kernel<1><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK);
+    k5_nv12map_kernel<1><<<kSMs, 256, kNvLutBytes, stream>>>(out, nh, ns, nv, kMadK, 0);
   else
-    k5_nv12map_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, kMadK);
+    k5_nv12map_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, kMadK, 0);
   return cudaGetLastError();
 }
 

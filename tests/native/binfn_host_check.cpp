@@ -60,7 +60,8 @@ int main(int argc, char** argv) {
     }
     // direct-offset codes: both B forms, offsets in range and multiples of 4
     const uint32_t dp = code_pair_dir_pre<0>(R, G, B, kMadK, i0, i1);
-    if (code_pair_dir_pre<1>(R, G, B, kMadK, i0, i1) != dp) {
+    if (code_pair_dir_pre<1>(R, G, B, kMadK, i0, i1) != dp ||
+        code_pair_dir_pre<2>(R, G, B, kMadK, i0, i1) != dp) {
       fprintf(stderr, "dir pre TBF mismatch\n");
       return 1;
     }

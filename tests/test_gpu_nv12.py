@@ -81,6 +81,23 @@ def test_nv12_scores_random(ctx, dev, W, H, n):
     _check(ctx, random_nv12(rng, n, H, W))
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_nv12_every_code_layout(dev, variant, monkeypatch):
+    """Every K1-NV12 code layout (CLIPDETECT_NV12_DIR: LUT codes, direct
+    offsets with each bank hash / table swizzle) gives the oracle's histograms
+    on random and structured surfaces, and the all-(Y,U,V) bin map."""
+    from paper_2503_12964_b200 import Ctx
+    monkeypatch.setenv("CLIPDETECT_NV12_DIR", str(variant))
+    c = Ctx(device=0)
+    rng = np.random.default_rng(100 + variant)
+    _check(c, random_nv12(rng, 3, 720, 1280))
+    _check(c, random_nv12(rng, 4, 240, 320, structured=True))
+    got = c.debug_nv12map().cpu().numpy()
+    want = yuv_bins()
+    assert np.array_equal(got[0], want) and np.array_equal(got[1], want)
+    c.close()
+
+
 def test_nv12_scores_structured(ctx, dev):
     rng = np.random.default_rng(11)
     _check(ctx, random_nv12(rng, 6, 240, 320, structured=True))
