@@ -37,8 +37,8 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
-  int nv12_dir = 1;  // K1-NV12 code layout: 0 = LUT codes, 1-3 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
-  int k1_cfg = 14;  // K1 launch configuration: LUT hue, staged lane-contiguous quads, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
+  int nv12_dir = 2;  // K1-NV12 code layout: 0 = LUT codes, 1-3 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
+  int k1_cfg = 49;  // K1 launch configuration: direct-offset codes, (d ^ na) bank hash, 3 x 36 KiB ring, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
   clip_stats stats{};

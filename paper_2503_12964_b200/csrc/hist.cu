@@ -63,8 +63,13 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 24, 12, 3, 0, 768}, {4, 1, 20, 12, 3, 0, 640},
                            {4, 1, 32, 10, 3, 1}, {2, 1, 32, 10, 3, 1, 1024},  // 32 warps, no producer
                            {4, 1, 16, 13, 3}, {4, 1, 16, 14, 3},  // lut 13/14: A, B on the FMA pipe
-                           {2, 1, 16, 10, 3, 0, 1024}, {2, 1, 32, 14, 3, 1, 1024}};
-constexpr int kNumCfgs = 47;
+                           {2, 1, 16, 10, 3, 0, 1024}, {2, 1, 32, 14, 3, 1, 1024},
+                           {3, 1, 16, 10, 3, 0, 768}, {4, 1, 16, 5, 3, 0, 640},  // 36 / 30 KiB stages
+                           {3, 1, 16, 9, 3, 0, 768}, {3, 1, 16, 6, 3, 0, 768},
+                           {4, 1, 16, 9, 3, 0, 640}, {3, 1, 16, 9, 4, 0, 768},
+                           {3, 1, 16, 15, 3, 0, 768}, {2, 1, 16, 9, 3, 0, 1024},  // lut 15: hash 3, swizzle 5
+                           {3, 1, 20, 9, 3, 0, 800}};
+constexpr int kNumCfgs = 56;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
@@ -72,14 +77,14 @@ __host__ __device__ constexpr int lut_swz(int lut) {
 }
 // lut 5-9: direct-offset codes (binfn.cuh code_pair_dir_pre; 6 = B on the FMA pipe),
 // bank hash of the table entries (binfn.cuh lut_entry_dir): 7 none, 8 na & 3,
-// 9 (d ^ na) & 3, 10 and 12 ((d >> 5) ^ na) & 3, 11 ((d >> 6) ^ d) & 3, otherwise d & 3
+// 9 and 15 (d ^ na) & 3, 10, 12-14 ((d >> 5) ^ na) & 3, 11 ((d >> 6) ^ d) & 3, otherwise d & 3
 // (tools/atoms_bank_sim.py)
 __host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
 __host__ __device__ constexpr int lut_hash(int lut) {
-  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
+  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 || lut == 15 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
 }
 // table swizzle multiplier of the direct-offset configs: lut 12, 14 = 5, else 4
-__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 || lut == 14 ? 5 : 4; }
+__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 || lut == 14 || lut == 15 ? 5 : 4; }
 // flags A, B on the FMA pipe (code_pair_dir_pre TBF): lut 6 -> B, lut 13, 14 -> A and B
 __host__ __device__ constexpr int lut_tbf(int lut) { return lut == 6 ? 1 : (lut == 13 || lut == 14 ? 2 : 0); }
 
@@ -588,7 +593,8 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
     K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27) K1_CASE(28) K1_CASE(29)
     K1_CASE(30) K1_CASE(31) K1_CASE(32) K1_CASE(33) K1_CASE(34) K1_CASE(35) K1_CASE(36)
     K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42) K1_CASE(43)
-    K1_CASE(44) K1_CASE(45) K1_CASE(46)
+    K1_CASE(44) K1_CASE(45) K1_CASE(46) K1_CASE(47) K1_CASE(48) K1_CASE(49) K1_CASE(50)
+    K1_CASE(51) K1_CASE(52) K1_CASE(53) K1_CASE(54) K1_CASE(55)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -650,7 +656,16 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 43>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 44>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 45>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 46>();
+  if ((e = configure_cfg<MODE, 46>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 47>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 48>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 49>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 50>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 51>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 52>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 53>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 54>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 55>();
 }
 
 }  // namespace

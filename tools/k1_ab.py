@@ -39,8 +39,18 @@ def main():
     res = {c: [] for c in cfgs}
     ref = None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        nvh = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        clk = lambda: pynvml.nvmlDeviceGetClockInfo(nvh, pynvml.NVML_CLOCK_SM)  # noqa: E731
+    except Exception:
+        clk = lambda: None  # noqa: E731
+    clocks = []
     for r in range(rounds):
-        for c in cfgs:
+        order = cfgs[r % len(cfgs):] + cfgs[:r % len(cfgs)]  # rotate: no fixed position in a round
+        clocks.append(clk())
+        for c in order:
             ctx = ctxs[c]
             with torch.cuda.stream(stream):
                 ctx.frame_scores(frames, hist=hist, want_l1=False, want_score=False)  # warm
@@ -57,7 +67,7 @@ def main():
                 res[c].append(float("nan"))
     out = {f"cfg{c}": {"median_gbs": round(statistics.median(x), 1), "all": [round(y, 1) for y in x]}
            for c, x in res.items()}
-    print(json.dumps({"frames": v.n, "bytes": frames.numel(), **out}))
+    print(json.dumps({"frames": v.n, "bytes": frames.numel(), "sm_mhz_per_round": clocks, **out}))
 
 
 if __name__ == "__main__":
