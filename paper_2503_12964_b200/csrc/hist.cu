@@ -2,23 +2,26 @@
 //
 // hist_t[b] = #{pixels of frame t with bin b} (reading O2; §2.1).
 //
-// B200 design:
-//  * persistent grid, 2 CTAs/SM; each CTA owns a CONTIGUOUS range of "stages"
-//    of the flattened (segment, frame, stage) space, so a CTA flushes its
-//    histogram only when its frame changes;
-//  * one producer lane streams each stage (<= kStageGroups x 48 B of one
-//    frame) HBM -> shared memory with a 1-D TMA bulk copy
-//    (cp.async.bulk ... mbarrier::complete_tx, L2 evict_first) into a
-//    kStages-deep ring; consumers signal "empty" per warp;
-//  * 8 consumer warps; each thread takes 48-byte groups (16 pixels, three
-//    conflict-free LDS.128), unpacks them into u16x2 pixel pairs and computes
-//    a per-pixel threshold CODE two pixels per instruction (binfn.cuh,
-//    code_pair: division-free sector form of the exact HSV bins), counted in
-//    a CTA-shared 2048-entry code histogram (atomicAdd(+1) ->
-//    ATOMS.POPC.INC, same-address lanes combined in hardware);
+// B200 design (the default launch configuration is cfg49):
+//  * persistent grid, one CTA per SM; each CTA owns a CONTIGUOUS range of
+//    "stages" of the flattened (segment, frame, stage) space, so a CTA flushes
+//    its histogram only when its frame changes;
+//  * one producer lane streams each stage (<= 768 x 48 B of one frame) HBM ->
+//    shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
+//    mbarrier::complete_tx, L2 evict_first) into a 3-deep ring; consumers
+//    signal "empty" per warp;
+//  * 16 consumer warps; each lane takes lane-contiguous 4-pixel quads (three
+//    conflict-free LDS.32), unpacks them into u16x2 pixel pairs and computes
+//    a per-pixel CODE two pixels per instruction (binfn.cuh
+//    code_pair_dir_pre: division-free sector form of the exact HSV bins with
+//    a 64 KiB hue table); the code of each lane is the byte offset of its
+//    entry in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm]
+//    -> ATOMS.POPC.INC, same-address lanes combined in hardware);
 //  * at a frame change the code histogram is mapped to the 162 bins
-//    (code_to_bin, a 2 KB smem table) and added to the global u32 histogram
-//    (integer adds: order-free, bit-deterministic).
+//    (code_to_bin_dir, an 8 KB smem table) and added to the global u32
+//    histogram (integer adds: order-free, bit-deterministic).
+// Older code layouts (cfg0-21: threshold codes, LUT codes) stay selectable
+// for tuning (CLIPDETECT_K1_CFG) and are parity-tested like the default.
 #include <stddef.h>
 
 #include "binfn.cuh"
