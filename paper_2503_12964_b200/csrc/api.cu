@@ -729,7 +729,11 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
   CKS(launch_k1(ctx, segs, mode));
   CKS(launch_k1_nv12(ctx, nsegs, mode));
 
-  // ---- K1: host / callback videos, chunk by chunk through two staging buffers
+  // ---- K1: host / callback videos through two staging buffers.  Chunks of
+  // consecutive videos are packed into one staging buffer (each chunk 16-B
+  // aligned: frame sizes are multiples of 48 B) and histogrammed by ONE K1
+  // launch over all of them (one segment per chunk), so batches of short
+  // videos are not launch- and tail-bound (SURVEY 8(d) "C5 batching").
   if (!streamed.empty()) {
     int64_t max_fb = 0;
     auto frame_bytes = [&](int32_t i) {
@@ -737,42 +741,72 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
     };
     for (int32_t i : streamed) max_fb = std::max<int64_t>(max_fb, frame_bytes(i));
     int64_t cf = chunk_frames > 0 ? chunk_frames : std::max<int64_t>(1, ((int64_t)1 << 30) / max_fb);
-    CKS(ensure(ctx, ctx->staging[0], cf * max_fb));
-    CKS(ensure(ctx, ctx->staging[1], cf * max_fb));
-    int chunk_i = 0;
-    for (int32_t i : streamed) {
-      const clip_video& v = videos[i];
-      const int64_t fb = frame_bytes(i);
-      for (int64_t t0 = 0; t0 < v.n_frames; t0 += cf, ++chunk_i) {
-        const int64_t m = std::min(cf, v.n_frames - t0);
-        const int b = chunk_i & 1;
-        uint8_t* dst = P<uint8_t>(ctx->staging[b]);
-        if (v.frames) {
-          CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->consumed[b], 0));
-          CK(cudaMemcpyAsync(dst, v.frames + t0 * fb, m * fb, cudaMemcpyHostToDevice,
-                             ctx->copy_stream));
-          CK(cudaEventRecord(ctx->copied[b], ctx->copy_stream));
-          CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[b], 0));
-          ctx->stats.memcpy_h2d += m * fb;
-        } else {
-          if (fill(user, i, t0, m, dst, reinterpret_cast<uintptr_t>(ctx->stream)) != 0)
-            return fail(ctx, CLIP_E_INVALID, "fill callback failed (video %d, frame %lld)", i,
-                        (long long)t0);
-        }
-        if (v.format == CLIP_FORMAT_NV12) {
-          std::vector<Nv12Seg> one(1);
-          one[0] = Nv12Seg{dst, d_hist + (vd[i].fbase + t0) * nbins, m, v.height, v.width, 0, 0, 0};
-          CKS(launch_k1_nv12(ctx, one, mode));
-        } else {
-          std::vector<HistSeg> one(1);
-          one[0].frames = dst;
-          one[0].hist = d_hist + (vd[i].fbase + t0) * nbins;
-          one[0].n_frames = m;
-          one[0].groups = vd[i].npix / 16;
-          CKS(launch_k1(ctx, one, mode));
-        }
-        CK(cudaEventRecord(ctx->consumed[b], ctx->stream));
+    const int64_t cap = cf * max_fb;  // staging bytes: every single chunk fits
+    CKS(ensure(ctx, ctx->staging[0], cap));
+    CKS(ensure(ctx, ctx->staging[1], cap));
+    struct Piece { int32_t i; int64_t t0, m; };
+    std::vector<Piece> pieces;
+    for (int32_t i : streamed)
+      for (int64_t t0 = 0; t0 < videos[i].n_frames; t0 += cf)
+        pieces.push_back(Piece{i, t0, std::min(cf, videos[i].n_frames - t0)});
+    int batch_i = 0;
+    for (size_t p0 = 0; p0 < pieces.size(); ++batch_i) {
+      // the batch: consecutive pieces of one format within the staging capacity
+      const bool nv12 = videos[pieces[p0].i].format == CLIP_FORMAT_NV12;
+      size_t p1 = p0;
+      int64_t used = 0;
+      while (p1 < pieces.size() &&
+             (videos[pieces[p1].i].format == CLIP_FORMAT_NV12) == nv12 &&
+             used + pieces[p1].m * frame_bytes(pieces[p1].i) <= cap) {
+        used += pieces[p1].m * frame_bytes(pieces[p1].i);
+        ++p1;
       }
+      const int b = batch_i & 1;
+      uint8_t* base = P<uint8_t>(ctx->staging[b]);
+      bool copies = false;
+      CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->consumed[b], 0));
+      std::vector<HistSeg> segs_b;
+      std::vector<Nv12Seg> nsegs_b;
+      int64_t off = 0;
+      for (size_t q = p0; q < p1; ++q) {
+        const Piece& pc = pieces[q];
+        const clip_video& v = videos[pc.i];
+        const int64_t fb = frame_bytes(pc.i);
+        uint8_t* dst = base + off;
+        if (v.frames) {
+          CK(cudaMemcpyAsync(dst, v.frames + pc.t0 * fb, pc.m * fb, cudaMemcpyHostToDevice,
+                             ctx->copy_stream));
+          ctx->stats.memcpy_h2d += pc.m * fb;
+          copies = true;
+        } else {
+          if (!copies) CK(cudaStreamWaitEvent(ctx->stream, ctx->consumed[b], 0));
+          if (fill(user, pc.i, pc.t0, pc.m, dst, reinterpret_cast<uintptr_t>(ctx->stream)) != 0)
+            return fail(ctx, CLIP_E_INVALID, "fill callback failed (video %d, frame %lld)", pc.i,
+                        (long long)pc.t0);
+        }
+        if (nv12) {
+          nsegs_b.push_back(Nv12Seg{dst, d_hist + (vd[pc.i].fbase + pc.t0) * nbins, pc.m, v.height,
+                                    v.width, 0, 0, 0});
+        } else {
+          HistSeg s{};
+          s.frames = dst;
+          s.hist = d_hist + (vd[pc.i].fbase + pc.t0) * nbins;
+          s.n_frames = pc.m;
+          s.groups = vd[pc.i].npix / 16;
+          segs_b.push_back(s);
+        }
+        off += pc.m * fb;
+      }
+      if (copies) {
+        CK(cudaEventRecord(ctx->copied[b], ctx->copy_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[b], 0));
+      }
+      if (nv12)
+        CKS(launch_k1_nv12(ctx, nsegs_b, mode));
+      else
+        CKS(launch_k1(ctx, segs_b, mode));
+      CK(cudaEventRecord(ctx->consumed[b], ctx->stream));
+      p0 = p1;
     }
   }
 

@@ -112,10 +112,10 @@ struct MadK {
   uint32_t sl4;   // 2^4
   uint32_t sl16;  // 2^16
   uint32_t sl20;  // 2^20
-  uint32_t four, neg4, neg6, neg7;
+  uint32_t four, neg4, neg6, neg7, neg3;
 };
 constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20,
-                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu, 0xFFFFFFF9u};
+                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu, 0xFFFFFFF9u, 0xFFFFFFFDu};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -327,9 +327,13 @@ CD_HD uint32_t lut_unswizzle_k(uint32_t b, uint32_t d, uint32_t ks) { return (b 
 // the two table indices.  TBF = 1 computes B (2: A and B) on the FMA pipe (two
 // IMADs each) instead of one IADD3 each on the ALU pipe.  KS = table swizzle multiplier (4 or 5):
 // na + KS d = sum + (KS - 1) max - (KS + 2) min.
-template <int TBF = 0, int KS = 4>
+// XU = 1: the lanes carry a per-pixel offset 256 X in their high byte (the same
+// X for the pixel's three channels, unpack4x): orderings, differences, d and the
+// table index are unchanged; the two terms that need the absolute max take the
+// offset back through their addends, kz = 2^10 + 256 X and km = -768 X.
+template <int TBF = 0, int KS = 4, int XU = 0>
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
-                                 uint32_t& i1) {
+                                 uint32_t& i1, uint32_t kz = 0u, uint32_t km = 0u) {
   static_assert(KS == 4 || KS == 5, "swizzle multiplier");
   const uint32_t mx = cd_max3_u16x2(R, G, B);
   const uint32_t mn = cd_min3_u16x2(R, G, B);
@@ -343,10 +347,10 @@ CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t tB = TBF ? cd_mad(B, k.neg1, cd_mad(G, k.one, 0x20002000u))
                           : G + 0x20002000u - B;                       // bit 13: g >= b
   const uint32_t tC = cd_mad(B, k.neg4, cd_mad(R, k.four, 0x40004000u));  // bit 14: r >= b
-  const uint32_t z1 = cd_mad(mx, k.neg1, 0x04000400u);
+  const uint32_t z1 = cd_mad(mx, k.neg1, XU ? kz : 0x04000400u);
   const uint32_t x1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10:  bit 10 = s1, < 2^11
   const uint32_t x2 = cd_mad(z1, k.one, x1);   // 3d - 2mx + 2^11: bit 11 = s2, < 2^12
-  const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8-9 of 3 max = v, < 2^10
+  const uint32_t m3 = cd_mad(mx, k.three, XU ? km : 0u);  // bits 8-9 of 3 max = v, < 2^10
   uint32_t p = cd_sel<0x04000400u>(x1, x2);  // bit 10 s1, bit 11 s2, bits 12-15 zero
   p = cd_sel<0x03000300u>(m3, p);
   p = cd_sel<0x10001000u>(tA, p);
@@ -436,6 +440,21 @@ CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_
 CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
                    uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23) {
   unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, kMadK);
+}
+
+// unpack4 without the two shifts: the high byte of every lane is a data byte X
+// of w1 (bytes 0 and 1: g1, b1), the same for the three channels of a pixel;
+// off = 256 X per lane for code_pair_dir_pre<.., XU = 1> (kz = off + 2^10, km = -3 off).
+CD_HD void unpack4x(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
+                    uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23, uint32_t& off) {
+  // w0 = [r0 g0 b0 r1], w1 = [g1 b1 r2 g2], w2 = [b2 r3 g3 b3]; X0 = w1.b0, X1 = w1.b1
+  R01 = cd_prmt(w0, w1, 0x5340u);
+  G01 = cd_prmt(w0, w1, 0x5441u);
+  B01 = cd_prmt(w0, w1, 0x5542u);
+  R23 = cd_prmt(w1, w2, 0x1502u);
+  G23 = cd_prmt(w1, w2, 0x1603u);
+  B23 = cd_prmt(w1, w2, 0x1704u);
+  off = cd_prmt(w1, 0u, 0x1404u);
 }
 
 // -------------------------------------------------- scalar forms (reference/tests)

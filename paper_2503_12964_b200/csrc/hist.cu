@@ -71,8 +71,9 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 16, 9, 3, 0, 768}, {3, 1, 16, 6, 3, 0, 768},
                            {4, 1, 16, 9, 3, 0, 640}, {3, 1, 16, 9, 4, 0, 768},
                            {3, 1, 16, 15, 3, 0, 768}, {2, 1, 16, 9, 3, 0, 1024},  // lut 15: hash 3, swizzle 5
-                           {3, 1, 20, 9, 3, 0, 800}};
-constexpr int kNumCfgs = 56;
+                           {3, 1, 20, 9, 3, 0, 800},
+                           {3, 1, 16, 16, 3, 0, 768}, {3, 1, 16, 17, 3, 0, 768}};  // unpack4x
+constexpr int kNumCfgs = 58;
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
@@ -84,12 +85,14 @@ __host__ __device__ constexpr int lut_swz(int lut) {
 // (tools/atoms_bank_sim.py)
 __host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
 __host__ __device__ constexpr int lut_hash(int lut) {
-  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 || lut == 15 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
+  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 || lut >= 15 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
 }
 // table swizzle multiplier of the direct-offset configs: lut 12, 14 = 5, else 4
 __host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 || lut == 14 || lut == 15 ? 5 : 4; }
-// flags A, B on the FMA pipe (code_pair_dir_pre TBF): lut 6 -> B, lut 13, 14 -> A and B
-__host__ __device__ constexpr int lut_tbf(int lut) { return lut == 6 ? 1 : (lut == 13 || lut == 14 ? 2 : 0); }
+// unpack without shifts (unpack4x, code_pair_dir_pre XU): lut 16 (hash 3), 17 (hash 3, TBF 1)
+__host__ __device__ constexpr int lut_xu(int lut) { return lut == 16 || lut == 17 ? 1 : 0; }
+// flags A, B on the FMA pipe (code_pair_dir_pre TBF): lut 6, 17 -> B, lut 13, 14 -> A and B
+__host__ __device__ constexpr int lut_tbf(int lut) { return lut == 6 || lut == 17 ? 1 : (lut == 13 || lut == 14 ? 2 : 0); }
 
 template <int STAGES, int LUT, int SG>
 struct K1Smem {
@@ -303,7 +306,7 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
 // entry goes into its atomic's address with one PRMT.
 // OCT = 1: a lane's quads come in adjacent pairs (24 bytes, three LDS.64):
 // quads 2j and 2j+1 of a lane are pixels [8 (q0 + j qstride), +8).
-template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0, int KS = 4>
+template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0, int KS = 4, int XU = 0>
 __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qstride, MadK mk) {
   uint32_t w[NQ][3];
   if constexpr (OCT) {
@@ -331,9 +334,18 @@ __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qs
 #pragma unroll
   for (int j = 0; j < NQ; ++j) {
     uint32_t R01, G01, B01, R23, G23, B23;
-    unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
-    pre[2 * j] = code_pair_dir_pre<TBF, KS>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-    pre[2 * j + 1] = code_pair_dir_pre<TBF, KS>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    if constexpr (XU) {  // no shifts in the unpack; the offset goes back through kz / km
+      uint32_t off;
+      unpack4x(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, off);
+      const uint32_t kz = cd_mad(off, mk.one, 0x04000400u), km = cd_mad(off, mk.neg3, 0u);
+      pre[2 * j] = code_pair_dir_pre<TBF, KS, 1>(R01, G01, B01, mk, ia[2 * j], ib[2 * j], kz, km);
+      pre[2 * j + 1] =
+          code_pair_dir_pre<TBF, KS, 1>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1], kz, km);
+    } else {
+      unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
+      pre[2 * j] = code_pair_dir_pre<TBF, KS>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+      pre[2 * j + 1] = code_pair_dir_pre<TBF, KS>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    }
   }
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
@@ -489,7 +501,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       if (nq == kQPL * kConsumers) {
         if constexpr (lut_dir(LUT))
           bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 0,
-                        lut_ks(LUT)>(
+                        lut_ks(LUT), lut_xu(LUT)>(
               buf, tid, kConsumers, mk);
         else
           bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
@@ -597,7 +609,7 @@ cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t to
     K1_CASE(30) K1_CASE(31) K1_CASE(32) K1_CASE(33) K1_CASE(34) K1_CASE(35) K1_CASE(36)
     K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42) K1_CASE(43)
     K1_CASE(44) K1_CASE(45) K1_CASE(46) K1_CASE(47) K1_CASE(48) K1_CASE(49) K1_CASE(50)
-    K1_CASE(51) K1_CASE(52) K1_CASE(53) K1_CASE(54) K1_CASE(55)
+    K1_CASE(51) K1_CASE(52) K1_CASE(53) K1_CASE(54) K1_CASE(55) K1_CASE(56) K1_CASE(57)
     default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   }
 #undef K1_CASE
@@ -668,7 +680,9 @@ cudaError_t configure_mode() {
   if ((e = configure_cfg<MODE, 52>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 53>()) != cudaSuccess) return e;
   if ((e = configure_cfg<MODE, 54>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 55>();
+  if ((e = configure_cfg<MODE, 55>()) != cudaSuccess) return e;
+  if ((e = configure_cfg<MODE, 56>()) != cudaSuccess) return e;
+  return configure_cfg<MODE, 57>();
 }
 
 }  // namespace

@@ -60,6 +60,15 @@ int main(int argc, char** argv) {
     }
     // direct-offset codes: both B forms, offsets in range and multiples of 4
     const uint32_t dp = code_pair_dir_pre<0>(R, G, B, kMadK, i0, i1);
+    // XU: a per-pixel offset 256 X in the high byte of every lane, taken back via kz / km
+    const uint32_t off = (((c * 7u) & 255u) << 8) | (((c * 13u + 5u) & 255u) << 24);
+    uint32_t x0, x1;
+    const uint32_t dpx = code_pair_dir_pre<0, 4, 1>(R + off, G + off, B + off, kMadK, x0, x1,
+                                                    off + 0x04000400u, off * 0xFFFFFFFDu);
+    if (dpx != dp || x0 != i0 || x1 != i1) {
+      fprintf(stderr, "dir pre XU mismatch\n");
+      return 1;
+    }
     if (code_pair_dir_pre<1>(R, G, B, kMadK, i0, i1) != dp ||
         code_pair_dir_pre<2>(R, G, B, kMadK, i0, i1) != dp) {
       fprintf(stderr, "dir pre TBF mismatch\n");
@@ -78,7 +87,7 @@ int main(int argc, char** argv) {
     e0[c] = (uint8_t)code_to_bin_dir(o0 >> 2);
     e1[c2] = (uint8_t)code_to_bin_dir(o1 >> 2);
   }
-  // unpack4 on pseudo-random bytes
+  // unpack4 / unpack4x on pseudo-random bytes
   uint32_t x = 12345u;
   for (int it = 0; it < 100000; ++it) {
     uint8_t by[12];
@@ -97,6 +106,18 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 6; ++i)
       if (got[i] != want[i]) {
         fprintf(stderr, "unpack4 mismatch %d: %08x vs %08x\n", i, got[i], want[i]);
+        return 1;
+      }
+    uint32_t X[6], off;
+    unpack4x(w[0], w[1], w[2], X[0], X[1], X[2], X[3], X[4], X[5], off);
+    const uint32_t xo = ((uint32_t)by[4] << 8) | ((uint32_t)by[5] << 24);  // 256 X: X0 = w1.b0, X1 = w1.b1
+    if (off != xo) {
+      fprintf(stderr, "unpack4x offset mismatch\n");
+      return 1;
+    }
+    for (int i = 0; i < 6; ++i)
+      if (X[i] != want[i] + xo) {
+        fprintf(stderr, "unpack4x mismatch %d: %08x vs %08x\n", i, X[i], want[i] + xo);
         return 1;
       }
   }

@@ -345,7 +345,7 @@ def test_invalid_arguments_fail_without_side_effects(ctx, dev):
 
 
 # ------------------------------------------------------------------ K1 launch configurations
-@pytest.mark.parametrize("cfg", list(range(56)))
+@pytest.mark.parametrize("cfg", list(range(58)))
 def test_every_k1_config_matches_oracle(dev, cfg, monkeypatch):
     """All K1 launch configurations (ring depth, CTAs/SM, warps, hue table,
     lane layout, producer scheme) give the oracle's histograms, incl. ragged
@@ -487,3 +487,46 @@ def test_python_shell_run(dev):
     nv = torch.from_numpy(synth.gen_nv12(v)).to(dev)
     assert run(nv, emb) == [10, 32, 53]
     assert run(frames) == [10, 21, 32, 43, 53]  # no embeddings: no merge
+
+
+# ------------------------------------------------------------------ packed streaming batches
+@pytest.mark.parametrize("chunk_frames", [0, 7, 50])
+def test_streamed_videos_packed_batches(ctx, dev, chunk_frames):
+    """Host and callback videos of mixed resolutions go through the staging
+    buffers as packed batches (several videos' chunks per K1 launch, one
+    segment each): every frame's histogram, L1 and every video's cuts equal
+    the oracle's, for chunk sizes that pack whole videos (0), many small pieces
+    (7) and pieces straddling batch boundaries (50)."""
+    vids = [manifest.subsample(v, 31 + 17 * k) for k, v in enumerate(manifest.c5_videos()[:6])]
+    tables = {i: torch_dev.frame_table(v, dev) for i, v in enumerate(vids)}
+    hosts = [synth.gen_frames(v) for v in vids]
+    items, refs = [], []
+    for i, v in enumerate(vids):
+        e_host = synth.gen_emb(v)
+        items.append({"n": v.n, "H": v.H, "W": v.W, "frames": hosts[i] if i % 3 == 2 else None,
+                      "id": i, "emb": torch.from_numpy(e_host).to(dev)})
+        refs.append(oracle.run_video(hosts[i], e_host))
+
+    def fill(vi, t0, n, dst, stream):
+        v = vids[vi]
+        return synth.dev_lib().synth_dev_gen_frames(v.seed, v.id, v.W, v.H, t0, n,
+                                                   tables[vi].data_ptr(), dst, stream)
+
+    F = sum(v.n for v in vids)
+    hist = torch.empty((F, 162), dtype=torch.int32, device=dev)
+    l1 = torch.empty(F, dtype=torch.int32, device=dev)
+    before = ctx.stats()["k1_launches"]
+    res = ctx.run_videos(items, fill=fill, chunk_frames=chunk_frames, hist=hist, l1=l1,
+                         want_cos=True)
+    launches = ctx.stats()["k1_launches"] - before
+    h, l = _u32(hist), _u32(l1)
+    f0 = 0
+    for r, ref, v in zip(res, refs, vids):
+        assert np.array_equal(h[f0:f0 + v.n], ref.hist)
+        assert np.array_equal(l[f0:f0 + v.n], ref.l1)
+        assert list(r.detected) == list(ref.detected)
+        assert list(r.final) == list(ref.final)
+        np.testing.assert_allclose(r.detected_cos, ref.cos, rtol=COS_RTOL, atol=1e-12)
+        f0 += v.n
+    pieces = sum(-(-v.n // (chunk_frames or v.n + 1)) for v in vids)
+    assert launches < pieces or chunk_frames == 0, (launches, pieces)  # chunks were packed

@@ -13,8 +13,10 @@ run() {  # name, port, args...
       --master-port $port bench.py --gpus $N "$@" > gpurun_out/$name.log 2>&1; echo "rc=$?" >> gpurun_out/$name.log
   fi
 }
+if [ -z "$ONLY_CONFIGS" ]; then
 run bench_n$N 29511 --steps 30 --warmup 3 ${BENCH_EXTRA}
 run bench_shard_n$N 29514 --shard-frames --steps 30 --warmup 3
+fi
 for c in ${CONFIGS:-C3 C4 C5}; do
   run bench_${c}_n$N 29512 --config $c --steps 2 --warmup 1
 done
