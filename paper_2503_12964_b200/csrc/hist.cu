@@ -687,14 +687,46 @@ cudaError_t configure_mode() {
 
 }  // namespace
 
+// K1_TU (build only): hist.cu is compiled once per mode (K1_TU = 0 fast +
+// shared entry points and K5, 1 generic, 2 read) so that the instantiations of
+// every launch configuration compile in parallel; undefined = everything here.
+#ifndef K1_TU
+#define K1_TU -1
+#endif
+#define K1_DECL_MODE(NAME)                                                                     \
+  cudaError_t k1_configure_##NAME();                                                           \
+  cudaError_t k1_launch_##NAME(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total,    \
+                               uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid, \
+                               cudaStream_t stream);
+#define K1_DEF_MODE(NAME, MODE)                                                                \
+  cudaError_t k1_configure_##NAME() { return configure_mode<MODE>(); }                         \
+  cudaError_t k1_launch_##NAME(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total,    \
+                               uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid, \
+                               cudaStream_t stream) {                                          \
+    return launch_mode<MODE>(cfg, d_segs, nseg, total, nh, ns, nv, sink, grid, stream);        \
+  }
+K1_DECL_MODE(fast)
+K1_DECL_MODE(generic)
+K1_DECL_MODE(read)
+#if K1_TU < 0 || K1_TU == 0
+K1_DEF_MODE(fast, kModeFast)
+#endif
+#if K1_TU < 0 || K1_TU == 1
+K1_DEF_MODE(generic, kModeGeneric)
+#endif
+#if K1_TU < 0 || K1_TU == 2
+K1_DEF_MODE(read, kModeRead)
+#endif
+
+#if K1_TU < 0 || K1_TU == 0
 int k1_stage_groups(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].sg : kStageGroups; }
 int k1_num_cfgs() { return kNumCfgs; }
 
 cudaError_t k1_configure() {
   cudaError_t e;
-  if ((e = configure_mode<kModeFast>()) != cudaSuccess) return e;
-  if ((e = configure_mode<kModeGeneric>()) != cudaSuccess) return e;
-  return configure_mode<kModeRead>();
+  if ((e = k1_configure_fast()) != cudaSuccess) return e;
+  if ((e = k1_configure_generic()) != cudaSuccess) return e;
+  return k1_configure_read();
 }
 
 int k1_grid(int cfg, int sm_count, int64_t total_stages) {
@@ -709,10 +741,10 @@ cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
                       uint32_t* sink, int grid, cudaStream_t stream) {
   if (total_stages <= 0) return cudaSuccess;
   if (mode == kModeFast)
-    return launch_mode<kModeFast>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    return k1_launch_fast(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
   if (mode == kModeGeneric)
-    return launch_mode<kModeGeneric>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-  return launch_mode<kModeRead>(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    return k1_launch_generic(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+  return k1_launch_read(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
 }
 
 // ---------------------------------------------------------------- K5 (test)
@@ -790,5 +822,7 @@ cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv
   }
   return cudaGetLastError();
 }
+
+#endif  // K1_TU
 
 }  // namespace clipdetect
