@@ -455,7 +455,7 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
   }
   if (const char* e = getenv("CLIPDETECT_NV12_DIR")) {
     const int c = atoi(e);
-    if (c >= 0 && c <= 3) ctx->nv12_dir = c;
+    if (c >= 0 && c <= 4) ctx->nv12_dir = c;
   }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       k1_nv12_configure() != cudaSuccess ||

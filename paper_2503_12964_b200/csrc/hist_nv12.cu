@@ -46,7 +46,8 @@ constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-fr
 
 // DIR > 0: direct-offset codes (binfn.cuh code_pair_dir_pre, 8192 entries):
 // 1 = bank hash d & 3, table swizzle multiplier 4; 2 = hash ((d >> 5) ^ na) & 3,
-// multiplier 4; 3 = that hash, multiplier 5 (CLIPDETECT_NV12_DIR selects)
+// multiplier 4; 3 = that hash, multiplier 5 (CLIPDETECT_NV12_DIR selects; 4 = layout 2
+// with two tiles per loop iteration)
 __host__ __device__ constexpr int nv_hash(int dir) { return dir == 1 ? 1 : 4; }
 __host__ __device__ constexpr int nv_ks(int dir) { return dir == 3 ? 5 : 4; }
 template <int DIR>
@@ -124,32 +125,40 @@ __device__ __forceinline__ void block_chroma(uint32_t uv, int k, int32_t& ruv, i
 // loads become LDS [index + imm] with no per-load base add.
 constexpr uint32_t kNvDynSmemBase = 0x400;
 
-// One 2 x 8 tile: Y row 0 (y0), Y row 1 (y1), UV (c): 8 pixel pairs.
-template <int DIR>
-__device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, MadK mk) {
-  uint32_t pre[8], ia[8], ib[8];
+// NT 2 x 8 tiles: Y row 0 (y0), Y row 1 (y1), UV (c) of each: 8 NT pixel
+// pairs, issued phase by phase (conversion + codes, table loads, atomics).
+template <int DIR, int NT = 1>
+__device__ __forceinline__ void nv_tiles(const uint2* y0s, const uint2* y1s, const uint2* cs,
+                                         char* hb, MadK mk) {
+  constexpr int P = 8 * NT;
+  uint32_t pre[P], ia[P], ib[P];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    int32_t ruv, guv, buv;
-    block_chroma(k < 2 ? c.x : c.y, k, ruv, guv, buv);
-    const uint32_t w0 = k < 2 ? y0.x : y0.y, w1 = k < 2 ? y1.x : y1.y;
-    const int o = 2 * (k & 1);
+  for (int t = 0; t < NT; ++t) {
+    const uint2 y0 = y0s[t], y1 = y1s[t], c = cs[t];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t w = r ? w1 : w0;
-      uint32_t R, G, B;
-      nv12_pair_rgb(__byte_perm(w, 0u, 0x4440u | o), __byte_perm(w, 0u, 0x4440u | (o + 1)), ruv,
-                    guv, buv, R, G, B);
-      if constexpr (DIR)
-        pre[2 * k + r] = code_pair_dir_pre<0, nv_ks(DIR)>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
-      else
-        pre[2 * k + r] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[2 * k + r], ib[2 * k + r]);
+    for (int k = 0; k < 4; ++k) {
+      int32_t ruv, guv, buv;
+      block_chroma(k < 2 ? c.x : c.y, k, ruv, guv, buv);
+      const uint32_t w0 = k < 2 ? y0.x : y0.y, w1 = k < 2 ? y1.x : y1.y;
+      const int o = 2 * (k & 1);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t w = r ? w1 : w0;
+        const int j = 8 * t + 2 * k + r;
+        uint32_t R, G, B;
+        nv12_pair_rgb(__byte_perm(w, 0u, 0x4440u | o), __byte_perm(w, 0u, 0x4440u | (o + 1)), ruv,
+                      guv, buv, R, G, B);
+        if constexpr (DIR)
+          pre[j] = code_pair_dir_pre<0, nv_ks(DIR)>(R, G, B, mk, ia[j], ib[j]);
+        else
+          pre[j] = code_pair_lut_pre<kNvSwz>(R, G, B, mk, ia[j], ib[j]);
+      }
     }
   }
-  uint32_t qa[8], qb[8];
+  uint32_t qa[P], qb[P];
   constexpr uint32_t lut_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem<DIR>, lut);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < P; ++j) {
     qa[j] = lds_u8(lut_s + ia[j]);
     qb[j] = lds_u8(lut_s + ib[j]);
   }
@@ -157,13 +166,13 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, M
     // ATOMS [offset + imm]: the histogram's shared-window address is a constant too
     constexpr uint32_t hist_s = kNvDynSmemBase + (uint32_t)offsetof(NvSmem<DIR>, hist);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < P; ++j) {
       asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(dir_off_lo(pre[j], qa[j])), "n"(hist_s) : "memory");
       asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(dir_off_hi(pre[j], qb[j])), "n"(hist_s) : "memory");
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < P; ++j) {
       const uint32_t code = code_pair_lut_post(pre[j], qa[j], qb[j], mk);
       atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_lo(code, mk)), 1u);
       atomicAdd(reinterpret_cast<uint32_t*>(hb + lut_off_hi(code, mk)), 1u);
@@ -171,7 +180,7 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, char* hb, M
   }
 }
 
-template <int MODE, int DIR>
+template <int MODE, int DIR, int NT = 1>
 __global__ void __launch_bounds__(kNvConsumers + 32, 1)
 k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                MadK mk_param, uint32_t* __restrict__ sink) {
@@ -269,8 +278,33 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const uint8_t* uvb = buf + 2 * nr * W;
     const int32_t nu = nr * wu;
     int32_t br = br0, cx = cx0;
+    auto step = [&]() {
+      cx += dr;
+      br += dq;
+      if (cx >= wu) {
+        cx -= wu;
+        ++br;
+      }
+    };
+    int32_t u = tid;
+    if constexpr (MODE == kModeFast && NT == 2) {
+      // two of this lane's tiles per iteration: 16 independent pixel-pair chains
 #pragma unroll 1
-    for (int32_t u = tid; u < nu; u += kNvConsumers) {
+      for (; u + kNvConsumers < nu; u += 2 * kNvConsumers) {
+        uint2 a[2], b[2], c[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const uint8_t* yp = buf + 2 * br * W + 8 * cx;
+          a[t] = *reinterpret_cast<const uint2*>(yp);
+          b[t] = *reinterpret_cast<const uint2*>(yp + W);
+          c[t] = *reinterpret_cast<const uint2*>(uvb + br * W + 8 * cx);
+          step();
+        }
+        nv_tiles<DIR, 2>(a, b, c, hb, mk);
+      }
+    }
+#pragma unroll 1
+    for (; u < nu; u += kNvConsumers) {
       const uint8_t* yp = buf + 2 * br * W + 8 * cx;
       const uint2 a = *reinterpret_cast<const uint2*>(yp);
       const uint2 b = *reinterpret_cast<const uint2*>(yp + W);
@@ -278,14 +312,9 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       if constexpr (MODE == kModeRead) {
         xacc ^= a.x ^ a.y ^ b.x ^ b.y ^ c.x ^ c.y;
       } else {
-        nv_tile<DIR>(a, b, c, hb, mk);
+        nv_tiles<DIR, 1>(&a, &b, &c, hb, mk);
       }
-      cx += dr;
-      br += dq;
-      if (cx >= wu) {
-        cx -= wu;
-        ++br;
-      }
+      step();
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -437,6 +466,9 @@ cudaError_t k1_nv12_configure() {
   if (e != cudaSuccess) return e;
   NV_CONF(kModeFast, 0) NV_CONF(kModeFast, 1) NV_CONF(kModeFast, 2) NV_CONF(kModeFast, 3)
   NV_CONF(kModeRead, 0)
+  e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
+  if (e != cudaSuccess) return e;
 #undef NV_CONF
   e = cudaFuncSetAttribute(k5_nv12map_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kNvLutBytes);
@@ -460,6 +492,9 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 2)
     k1_nv12_kernel<kModeFast, 2><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 4)  // layout 2, two tiles per iteration
+    k1_nv12_kernel<kModeFast, 2, 2><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 3)
     k1_nv12_kernel<kModeFast, 3><<<grid, kNvConsumers + 32, sizeof(NvSmem<3>), stream>>>(
