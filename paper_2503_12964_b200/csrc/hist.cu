@@ -24,6 +24,8 @@
 // for tuning (CLIPDETECT_K1_CFG) and are parity-tested like the default.
 #include <stddef.h>
 
+#include <utility>
+
 #include "binfn.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -73,7 +75,7 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 16, 15, 3, 0, 768}, {2, 1, 16, 9, 3, 0, 1024},  // lut 15: hash 3, swizzle 5
                            {3, 1, 20, 9, 3, 0, 800},
                            {3, 1, 16, 16, 3, 0, 768}, {3, 1, 16, 17, 3, 0, 768}};  // unpack4x
-constexpr int kNumCfgs = 58;
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
 __host__ __device__ constexpr int lut_swz(int lut) {
@@ -595,24 +597,25 @@ cudaError_t launch_cfg(const HistSeg* d_segs, int32_t nseg, int64_t total_stages
   return cudaGetLastError();
 }
 
+// cfg (runtime) -> launch_cfg<MODE, cfg> over every configuration; unknown -> 0
+template <int MODE, int... C>
+cudaError_t launch_any(std::integer_sequence<int, C...>, int cfg, const HistSeg* d_segs,
+                       int32_t nseg, int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
+                       uint32_t* sink, int grid, cudaStream_t stream) {
+  cudaError_t e = cudaErrorInvalidValue;
+  const bool hit = ((cfg == C ? (e = launch_cfg<MODE, C>(d_segs, nseg, total_stages, nh, ns, nv,
+                                                          sink, grid, stream),
+                                 true)
+                              : false) || ...);
+  return hit ? e : launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+}
+
 template <int MODE>
 cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
                         uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
                         cudaStream_t stream) {
-#define K1_CASE(c) \
-  case c: return launch_cfg<MODE, c>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-  switch (cfg) {
-    K1_CASE(1) K1_CASE(2) K1_CASE(3) K1_CASE(4) K1_CASE(5) K1_CASE(6) K1_CASE(7) K1_CASE(8)
-    K1_CASE(9) K1_CASE(10) K1_CASE(11) K1_CASE(12) K1_CASE(13) K1_CASE(14) K1_CASE(15)
-    K1_CASE(16) K1_CASE(17) K1_CASE(18) K1_CASE(19) K1_CASE(20) K1_CASE(21) K1_CASE(22)
-    K1_CASE(23) K1_CASE(24) K1_CASE(25) K1_CASE(26) K1_CASE(27) K1_CASE(28) K1_CASE(29)
-    K1_CASE(30) K1_CASE(31) K1_CASE(32) K1_CASE(33) K1_CASE(34) K1_CASE(35) K1_CASE(36)
-    K1_CASE(37) K1_CASE(38) K1_CASE(39) K1_CASE(40) K1_CASE(41) K1_CASE(42) K1_CASE(43)
-    K1_CASE(44) K1_CASE(45) K1_CASE(46) K1_CASE(47) K1_CASE(48) K1_CASE(49) K1_CASE(50)
-    K1_CASE(51) K1_CASE(52) K1_CASE(53) K1_CASE(54) K1_CASE(55) K1_CASE(56) K1_CASE(57)
-    default: return launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-  }
-#undef K1_CASE
+  return launch_any<MODE>(std::make_integer_sequence<int, kNumCfgs>{}, cfg, d_segs, nseg,
+                          total_stages, nh, ns, nv, sink, grid, stream);
 }
 
 template <int MODE, int C>
@@ -622,67 +625,17 @@ cudaError_t configure_cfg() {
                               (int)K::smem());
 }
 
+// the shared-memory opt-in of every configuration's kernel; first error wins
+template <int MODE, int... C>
+cudaError_t configure_all(std::integer_sequence<int, C...>) {
+  cudaError_t e = cudaSuccess;
+  ((e == cudaSuccess ? (e = configure_cfg<MODE, C>(), 0) : 0), ...);
+  return e;
+}
+
 template <int MODE>
 cudaError_t configure_mode() {
-  cudaError_t e;
-  if ((e = configure_cfg<MODE, 0>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 1>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 2>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 3>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 4>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 5>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 6>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 7>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 8>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 9>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 10>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 11>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 12>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 13>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 14>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 15>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 16>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 17>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 18>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 19>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 20>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 21>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 22>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 23>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 24>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 25>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 26>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 27>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 28>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 29>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 30>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 31>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 32>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 33>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 34>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 35>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 36>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 37>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 38>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 39>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 40>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 41>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 42>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 43>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 44>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 45>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 46>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 47>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 48>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 49>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 50>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 51>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 52>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 53>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 54>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 55>()) != cudaSuccess) return e;
-  if ((e = configure_cfg<MODE, 56>()) != cudaSuccess) return e;
-  return configure_cfg<MODE, 57>();
+  return configure_all<MODE>(std::make_integer_sequence<int, kNumCfgs>{});
 }
 
 }  // namespace
