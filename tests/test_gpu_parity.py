@@ -530,3 +530,23 @@ def test_streamed_videos_packed_batches(ctx, dev, chunk_frames):
         f0 += v.n
     pieces = sum(-(-v.n // (chunk_frames or v.n + 1)) for v in vids)
     assert launches < pieces or chunk_frames == 0, (launches, pieces)  # chunks were packed
+
+
+@pytest.mark.parametrize("cfg", [None, 14, 22, 56])
+def test_k1_every_colour_frame(dev, cfg, monkeypatch):
+    """One 4096 x 4096 frame holding each of the 2^24 colours once, through K1's
+    fast path (default launch configuration, the LUT-code cfg14, the first
+    direct-offset layout and the shift-free unpack): the histogram equals the
+    oracle's bin table counted per bin — every code, table entry, bank hash and
+    the frame flush exercised at once."""
+    from paper_2503_12964_b200 import Ctx
+    if cfg is not None:
+        monkeypatch.setenv("CLIPDETECT_K1_CFG", str(cfg))
+    c = Ctx(device=0)
+    col = torch.arange(1 << 24, dtype=torch.int32, device=dev)
+    frame = torch.stack([(col >> 16) & 255, (col >> 8) & 255, col & 255], dim=-1)
+    frame = frame.to(torch.uint8).reshape(1, 4096, 4096, 3)
+    hist, _, _ = c.frame_scores(frame)
+    want = np.bincount(oracle.bin_table(), minlength=162).astype(np.uint32)
+    assert np.array_equal(_u32(hist)[0], want)
+    c.close()

@@ -30,7 +30,9 @@ def main():
         os.environ["CLIPDETECT_K1_CFG"] = str(c)
         ctxs[c] = Ctx(device=0, stream=stream)
     os.environ.pop("CLIPDETECT_K1_CFG", None)
-    v = manifest.subsample(manifest.c2_video(0), n) if n < 18000 else manifest.c2_video(0)
+    which = os.environ.get("K1_VIDEO", "c2")  # c2: the C2 video; c3: C3 video 0 (1080p, fades, flashes)
+    base = manifest.c3_videos()[0] if which == "c3" else manifest.c2_video(0)
+    v = manifest.subsample(base, n) if n < base.n else base
     table = torch_dev.frame_table(v, dev)
     frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
     torch_dev.gen_frames(v, table, frames)
@@ -67,7 +69,7 @@ def main():
                 res[c].append(float("nan"))
     out = {f"cfg{c}": {"median_gbs": round(statistics.median(x), 1), "all": [round(y, 1) for y in x]}
            for c, x in res.items()}
-    print(json.dumps({"frames": v.n, "bytes": frames.numel(), "sm_mhz_per_round": clocks, **out}))
+    print(json.dumps({"video": which, "frames": v.n, "bytes": frames.numel(), "sm_mhz_per_round": clocks, **out}))
 
 
 if __name__ == "__main__":
