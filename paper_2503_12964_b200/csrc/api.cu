@@ -38,7 +38,7 @@ struct clip_ctx {
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
   int nv12_dir = 2;  // K1-NV12 code layout: 0 = LUT codes, 1-3 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
-  int k1_cfg = 49;  // K1 launch configuration: direct-offset codes, (d ^ na) bank hash, 3 x 36 KiB ring, 16 consumer warps (CLIPDETECT_K1_CFG overrides)
+  int k1_cfg = 55;  // K1 launch configuration: direct-offset codes, (d ^ na) bank hash, 3 x 37.5 KiB ring, 20 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
   clip_stats stats{};
