@@ -2,15 +2,15 @@
 //
 // hist_t[b] = #{pixels of frame t with bin b} (reading O2; §2.1).
 //
-// B200 design (the default launch configuration is cfg49):
+// B200 design (the default launch configuration is cfg55):
 //  * persistent grid, one CTA per SM; each CTA owns a CONTIGUOUS range of
 //    "stages" of the flattened (segment, frame, stage) space, so a CTA flushes
 //    its histogram only when its frame changes;
-//  * one producer lane streams each stage (<= 768 x 48 B of one frame) HBM ->
+//  * one producer lane streams each stage (<= 800 x 48 B of one frame) HBM ->
 //    shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
 //    mbarrier::complete_tx, L2 evict_first) into a 3-deep ring; consumers
 //    signal "empty" per warp;
-//  * 16 consumer warps; each lane takes lane-contiguous 4-pixel quads (three
+//  * 20 consumer warps; each lane takes lane-contiguous 4-pixel quads (three
 //    conflict-free LDS.32), unpacks them into u16x2 pixel pairs and computes
 //    a per-pixel CODE two pixels per instruction (binfn.cuh
 //    code_pair_dir_pre: division-free sector form of the exact HSV bins with
