@@ -75,7 +75,8 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 16, 15, 3, 0, 768}, {2, 1, 16, 9, 3, 0, 1024},  // lut 15: hash 3, swizzle 5
                            {3, 1, 20, 9, 3, 0, 800},
                            {3, 1, 16, 16, 3, 0, 768}, {3, 1, 16, 17, 3, 0, 768},  // unpack4x
-                           {3, 1, 20, 5, 3, 0, 800}};  // d & 3 hash, 20 consumer warps
+                           {3, 1, 20, 5, 3, 0, 800},   // d & 3 hash, 20 consumer warps
+                           {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768}};  // 24 consumer warps
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
