@@ -76,7 +76,9 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 20, 9, 3, 0, 800},
                            {3, 1, 16, 16, 3, 0, 768}, {3, 1, 16, 17, 3, 0, 768},  // unpack4x
                            {3, 1, 20, 5, 3, 0, 800},   // d & 3 hash, 20 consumer warps
-                           {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768}};  // 24 consumer warps
+                           {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768},  // 24 consumer warps
+                           {4, 1, 20, 9, 5, 0, 640}, {3, 1, 20, 9, 5, 0, 640},  // quad 5: LDS.128 groups
+                           {2, 1, 20, 9, 5, 0, 1280}, {4, 1, 16, 9, 5, 0, 512}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
@@ -313,7 +315,19 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
 template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0, int KS = 4, int XU = 0>
 __device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qstride, MadK mk) {
   uint32_t w[NQ][3];
-  if constexpr (OCT) {
+  if constexpr (OCT == 2) {
+    // a lane's quads come in groups of four (48 bytes, three LDS.128): quads
+    // 4j..4j+3 are pixels [16 (q0 + j qstride), +16); a quarter-warp's 8 lanes
+    // at a 48-byte stride cover 32 distinct banks (conflict-free)
+#pragma unroll
+    for (int j = 0; j < NQ / 4; ++j) {
+      const uint4* p = reinterpret_cast<const uint4*>(buf + (q0 + j * qstride) * 48);
+      const uint4 a = p[0], b = p[1], c = p[2];
+      const uint32_t v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int k = 0; k < 12; ++k) w[4 * j + k / 3][k % 3] = v[k];
+    }
+  } else if constexpr (OCT) {
 #pragma unroll
     for (int j = 0; j < NQ / 2; ++j) {
       const uint2* p = reinterpret_cast<const uint2*>(buf + (q0 + j * qstride) * 24);
@@ -489,13 +503,14 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       const int nq = ng * 4;
 #pragma unroll 2
       for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
-    } else if constexpr (QUAD == 4 && MODE == kModeFast && lut_dir(LUT)) {
-      // lane-contiguous octets (24 bytes: three LDS.64), direct-offset codes
+    } else if constexpr ((QUAD == 4 || QUAD == 5) && MODE == kModeFast && lut_dir(LUT)) {
+      // lane-contiguous octets (QUAD 4: 24 bytes, three LDS.64) or 16-pixel
+      // groups (QUAD 5: 48 bytes, three LDS.128), direct-offset codes
       constexpr int kQPL = 4 * SG / kConsumers;
       const int nq = ng * 4;
       if (nq == kQPL * kConsumers) {
-        bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 1, lut_ks(LUT)>(
-            buf, tid, kConsumers, mk);
+        bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s,
+                      QUAD == 5 ? 2 : 1, lut_ks(LUT)>(buf, tid, kConsumers, mk);
       } else {
         for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
       }
