@@ -47,7 +47,8 @@ constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-fr
 // DIR > 0: direct-offset codes (binfn.cuh code_pair_dir_pre, 8192 entries):
 // 1 = bank hash d & 3, table swizzle multiplier 4; 2 = hash ((d >> 5) ^ na) & 3,
 // multiplier 4; 3 = that hash, multiplier 5 (CLIPDETECT_NV12_DIR selects; 4 = layout 2
-// with two tiles per loop iteration)
+// with two tiles per loop iteration; 5 = layout 2 with the lane -> unit map rotated by
+// two warps per stage, see ROT below)
 __host__ __device__ constexpr int nv_hash(int dir) { return dir == 1 ? 1 : 4; }
 __host__ __device__ constexpr int nv_ks(int dir) { return dir == 3 ? 5 : 4; }
 template <int DIR>
@@ -180,7 +181,13 @@ __device__ __forceinline__ void nv_tiles(const uint2* y0s, const uint2* y1s, con
   }
 }
 
-template <int MODE, int DIR, int NT = 1>
+// ROT = 1: a stage holds nu = R * W / 8 units (960 at 720p, 1080p and 4K) for 512
+// lanes, so 448 lanes take two units and 64 take one.  Without rotation the
+// one-unit lanes are always warps 14 and 15 (schedulers 2 and 3), and schedulers
+// 0 and 1 carry 8 of the stage's 30 warp-units against 7.  Rotating the lane ->
+// unit map by 64 lanes per stage moves the one-unit pair over warps (12, 13),
+// (10, 11), ...: every scheduler carries 15 warp-units per two stages.
+template <int MODE, int DIR, int NT = 1, int ROT = 0>
 __global__ void __launch_bounds__(kNvConsumers + 32, 1)
 k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                MadK mk_param, uint32_t* __restrict__ sink) {
@@ -277,7 +284,13 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const uint8_t* buf = sm.buf[slot];
     const uint8_t* uvb = buf + 2 * nr * W;
     const int32_t nu = nr * wu;
-    int32_t br = br0, cx = cx0;
+    int32_t br = br0, cx = cx0, u = tid;
+    if constexpr (ROT) {
+      static_assert((kNvConsumers & (kNvConsumers - 1)) == 0 && kNvConsumers == 512, "rotation period");
+      u = (tid + 64 * (i & 7)) & (kNvConsumers - 1);  // virtual lane of this stage
+      br = u / wu;
+      cx = u - br * wu;
+    }
     auto step = [&]() {
       cx += dr;
       br += dq;
@@ -286,7 +299,6 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
         ++br;
       }
     };
-    int32_t u = tid;
     if constexpr (MODE == kModeFast && NT == 2) {
       // two of this lane's tiles per iteration: 16 independent pixel-pair chains
 #pragma unroll 1
@@ -469,6 +481,9 @@ cudaError_t k1_nv12_configure() {
   e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 1, 1>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
+  if (e != cudaSuccess) return e;
 #undef NV_CONF
   e = cudaFuncSetAttribute(k5_nv12map_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kNvLutBytes);
@@ -495,6 +510,9 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 4)  // layout 2, two tiles per iteration
     k1_nv12_kernel<kModeFast, 2, 2><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 5)  // layout 2, rotated lane -> unit map
+    k1_nv12_kernel<kModeFast, 2, 1, 1><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 3)
     k1_nv12_kernel<kModeFast, 3><<<grid, kNvConsumers + 32, sizeof(NvSmem<3>), stream>>>(
