@@ -37,7 +37,7 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
-  int nv12_dir = 5;  // K1-NV12 code layout: 0 = LUT codes, 1-5 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
+  int nv12_dir = 6;  // K1-NV12 code layout: 0 = LUT codes, 1-7 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
   int k1_cfg = 55;  // K1 launch configuration: direct-offset codes, (d ^ na) bank hash, 3 x 37.5 KiB ring, 20 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
@@ -455,7 +455,7 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
   }
   if (const char* e = getenv("CLIPDETECT_NV12_DIR")) {
     const int c = atoi(e);
-    if (c >= 0 && c <= 5) ctx->nv12_dir = c;
+    if (c >= 0 && c <= 7) ctx->nv12_dir = c;
   }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       k1_nv12_configure() != cudaSuccess ||

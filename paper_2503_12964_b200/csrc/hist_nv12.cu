@@ -48,7 +48,7 @@ constexpr int kNvSwz = 3;  // table swizzle (binfn.cuh lut_swizzle): conflict-fr
 // 1 = bank hash d & 3, table swizzle multiplier 4; 2 = hash ((d >> 5) ^ na) & 3,
 // multiplier 4; 3 = that hash, multiplier 5 (CLIPDETECT_NV12_DIR selects; 4 = layout 2
 // with two tiles per loop iteration; 5 = layout 2 with the lane -> unit map rotated by
-// two warps per stage, see ROT below)
+// two warps per stage, see ROT below; 6 / 7 = 5 with 20 / 24 consumer warps)
 __host__ __device__ constexpr int nv_hash(int dir) { return dir == 1 ? 1 : 4; }
 __host__ __device__ constexpr int nv_ks(int dir) { return dir == 3 ? 5 : 4; }
 template <int DIR>
@@ -186,11 +186,13 @@ __device__ __forceinline__ void nv_tiles(const uint2* y0s, const uint2* y1s, con
 // one-unit lanes are always warps 14 and 15 (schedulers 2 and 3), and schedulers
 // 0 and 1 carry 8 of the stage's 30 warp-units against 7.  Rotating the lane ->
 // unit map by 64 lanes per stage moves the one-unit pair over warps (12, 13),
-// (10, 11), ...: every scheduler carries 15 warp-units per two stages.
-template <int MODE, int DIR, int NT = 1, int ROT = 0>
-__global__ void __launch_bounds__(kNvConsumers + 32, 1)
+// (10, 11), ...: every scheduler carries 15 warp-units per two stages.  NW =
+// consumer warps (layout 6: 20, 10 of them take two units; layout 7: 24, 6 of them).
+template <int MODE, int DIR, int NT = 1, int ROT = 0, int NW = kNvWarps>
+__global__ void __launch_bounds__(NW * 32 + 32, 1)
 k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_stages,
                MadK mk_param, uint32_t* __restrict__ sink) {
+  constexpr int kNvConsumers = NW * 32;  // this instance's consumer lanes
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using Smem = NvSmem<DIR>;
   constexpr int kEntries = Smem::kEntries;
@@ -220,7 +222,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kNvStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kNvWarps);
+      mbar_init(&sm.empty[i], NW);
     }
     fence_mbar_init();
   }
@@ -228,7 +230,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
   if (s_begin >= s_end) return;
   const int32_t n = (int32_t)(s_end - s_begin);
 
-  if (warp == kNvWarps) {
+  if (warp == NW) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -286,8 +288,8 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const int32_t nu = nr * wu;
     int32_t br = br0, cx = cx0, u = tid;
     if constexpr (ROT) {
-      static_assert((kNvConsumers & (kNvConsumers - 1)) == 0 && kNvConsumers == 512, "rotation period");
-      u = (tid + 64 * (i & 7)) & (kNvConsumers - 1);  // virtual lane of this stage
+      static_assert(kNvConsumers % 64 == 0, "rotation by two warps");
+      u = (tid + 64 * (i % (kNvConsumers / 64))) % kNvConsumers;  // virtual lane of this stage
       br = u / wu;
       cx = u - br * wu;
     }
@@ -484,6 +486,12 @@ cudaError_t k1_nv12_configure() {
   e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 1, 1>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 1, 1, 20>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k1_nv12_kernel<kModeFast, 2, 1, 1, 24>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(NvSmem<2>));
+  if (e != cudaSuccess) return e;
 #undef NV_CONF
   e = cudaFuncSetAttribute(k5_nv12map_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kNvLutBytes);
@@ -513,6 +521,12 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 5)  // layout 2, rotated lane -> unit map
     k1_nv12_kernel<kModeFast, 2, 1, 1><<<grid, kNvConsumers + 32, sizeof(NvSmem<2>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 6)  // layout 5 with 20 consumer warps
+    k1_nv12_kernel<kModeFast, 2, 1, 1, 20><<<grid, 20 * 32 + 32, sizeof(NvSmem<2>), stream>>>(
+        d_segs, nseg, total, kMadK, sink);
+  else if (mode == kModeFast && dir == 7)  // layout 5 with 24 consumer warps
+    k1_nv12_kernel<kModeFast, 2, 1, 1, 24><<<grid, 24 * 32 + 32, sizeof(NvSmem<2>), stream>>>(
         d_segs, nseg, total, kMadK, sink);
   else if (mode == kModeFast && dir == 3)
     k1_nv12_kernel<kModeFast, 3><<<grid, kNvConsumers + 32, sizeof(NvSmem<3>), stream>>>(

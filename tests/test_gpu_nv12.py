@@ -81,7 +81,7 @@ def test_nv12_scores_random(ctx, dev, W, H, n):
     _check(ctx, random_nv12(rng, n, H, W))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_nv12_every_code_layout(dev, variant, monkeypatch):
     """Every K1-NV12 code layout (CLIPDETECT_NV12_DIR: LUT codes, direct
     offsets with each bank hash / table swizzle) gives the oracle's histograms
