@@ -78,7 +78,8 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {3, 1, 20, 5, 3, 0, 800},   // d & 3 hash, 20 consumer warps
                            {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768},  // 24 consumer warps
                            {4, 1, 20, 9, 5, 0, 640}, {3, 1, 20, 9, 5, 0, 640},  // quad 5: LDS.128 groups
-                           {2, 1, 20, 9, 5, 0, 1280}, {4, 1, 16, 9, 5, 0, 512}};
+                           {2, 1, 20, 9, 5, 0, 1280}, {4, 1, 16, 9, 5, 0, 512},
+                           {4, 1, 20, 9, 3, 0, 640}};  // 4-deep ring, 4 quads per lane
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
