@@ -1,8 +1,11 @@
 #!/bin/bash
-# Experiment build (tools only): K1-NV12 with 30 KiB stages (R = floor(10240 / W) chroma
-# rows: 8 at 720p, i.e. 1280 tiles = exactly 2 per lane of 20 warps).  CLIPDETECT_LIB=tools/libclipdetect_nv30k.so
+# Experiment builds (tools only) of K1-NV12 ring shapes; CLIPDETECT_LIB=tools/libclipdetect_<tag>.so
+#   nv30k: 4 x 30 KiB (R = floor(10240 / W); now the default)   nv3x40k: 3 x 40 KiB (R = floor(13653 / W))
 set -e
 cd "$(dirname "$0")/../paper_2503_12964_b200/csrc"
 SRC="hist.cu hist_nv12.cu cuts.cu merge.cu sample.cu api.cu"
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared"
-nvcc $F -DCLIPDETECT_NV_STAGE_BYTES=30720 -o ../../tools/libclipdetect_nv30k.so $SRC
+case "${1:-nv3x40k}" in
+  nv30k) nvcc $F -DCLIPDETECT_NV_STAGE_BYTES=30720 -o ../../tools/libclipdetect_nv30k.so $SRC ;;
+  nv3x40k) nvcc $F -DCLIPDETECT_NV_STAGES=3 -DCLIPDETECT_NV_STAGE_BYTES=40960 -o ../../tools/libclipdetect_nv3x40k.so $SRC ;;
+esac
