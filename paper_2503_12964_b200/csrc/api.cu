@@ -985,7 +985,7 @@ int clip_debug_read_roofline_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t 
   CKS(check_ctx(ctx));
   CKS(validate_frames(ctx, frames, n_frames, height, width, false, CLIP_FORMAT_NV12));
   if (width % 16 != 0 || nv12_stage_rows(width) < 1)
-    return fail(ctx, CLIP_E_INVALID, "NV12 read roofline needs width %% 16 == 0 and <= 13648");
+    return fail(ctx, CLIP_E_INVALID, "NV12 read roofline needs width %% 16 == 0 and <= 20480");
   std::vector<Nv12Seg> segs(1);
   segs[0] = Nv12Seg{frames, nullptr, n_frames, height, width, 0, 0, 0};
   return launch_k1_nv12(ctx, segs, kModeRead);

@@ -12,7 +12,7 @@
 // B200 design (same skeleton as hist.cu K1):
 //  * persistent grid, one CTA per SM, contiguous ranges of "stages" of the
 //    flattened (segment, frame, stage) space; a stage is R chroma-block rows of
-//    one frame (R = floor(13653 / W)): the 2R Y rows and the R UV rows are two
+//    one frame (R = floor(20480 / W)): the 2R Y rows and the R UV rows are two
 //    contiguous byte ranges, moved by two 1-D TMA bulk copies completing on
 //    one mbarrier into a 4-deep ring of 24 KiB slots;
 //  * 16 consumer warps; a work unit is a 2 x 8 pixel tile (two LDS.64 of Y,
@@ -22,7 +22,7 @@
 //    VIMNMX.S16x2.RELU saturation) and then coded exactly like K1's LUT
 //    variant (code_pair_lut_pre / post, 64 KiB hue table, ATOMS.POPC.INC into
 //    a 5120-entry code histogram, code -> bin at the frame flush).
-// Fast path: 18x3x3 bins, W % 16 == 0, W <= 13648.  Anything else runs the
+// Fast path: 18x3x3 bins, W % 16 == 0, W <= 20480.  Anything else runs the
 // plain generic kernel at the bottom of this file (same conversion, direct
 // global loads, bin_generic).
 #include <stddef.h>
@@ -38,13 +38,13 @@ namespace clipdetect {
 namespace {
 
 #ifndef CLIPDETECT_NV_STAGES  // experiment builds (tools/) may override
-#define CLIPDETECT_NV_STAGES 3
+#define CLIPDETECT_NV_STAGES 2
 #endif
 constexpr int kNvStages = CLIPDETECT_NV_STAGES;
 #ifndef CLIPDETECT_NV_STAGE_BYTES  // experiment builds (tools/) may override
-#define CLIPDETECT_NV_STAGE_BYTES 40960
+#define CLIPDETECT_NV_STAGE_BYTES 61440
 #endif
-constexpr int kNvStageBytes = CLIPDETECT_NV_STAGE_BYTES;  // 3 * R * W <= 40960  <=>  R * W <= 13653
+constexpr int kNvStageBytes = CLIPDETECT_NV_STAGE_BYTES;  // 3 * R * W <= 61440  <=>  R * W <= 20480
 constexpr int kNvWarps = 16;
 constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvLutBytes = 65536;

@@ -74,7 +74,7 @@ def _check(ctx, host, p=oracle.Params()):
 @pytest.mark.parametrize("W,H,n", [(1280, 720, 3), (1920, 1080, 2), (16, 2, 9), (64, 4, 5),
                                    (848, 480, 4), (3840, 16, 2), (8192, 4, 2), (32, 200, 3),
                                    (40, 36, 4), (854, 480, 2), (8208, 4, 1), (2, 16, 3),
-                                   (10240, 4, 2), (13648, 4, 1), (13664, 4, 1)])
+                                   (10240, 4, 2), (13648, 4, 1), (20480, 2, 1), (20496, 2, 1)])
 def test_nv12_scores_random(ctx, dev, W, H, n):
     rng = np.random.default_rng(W * 31 + H + n)
     if (H * W) % 32:
