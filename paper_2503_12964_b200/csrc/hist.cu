@@ -79,7 +79,8 @@ constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6
                            {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768},  // 24 consumer warps
                            {4, 1, 20, 9, 5, 0, 640}, {3, 1, 20, 9, 5, 0, 640},  // quad 5: LDS.128 groups
                            {2, 1, 20, 9, 5, 0, 1280}, {4, 1, 16, 9, 5, 0, 512},
-                           {4, 1, 20, 9, 3, 0, 640}};  // 4-deep ring, 4 quads per lane
+                           {4, 1, 20, 9, 3, 0, 640},   // 4-deep ring, 4 quads per lane
+                           {2, 1, 20, 9, 3, 0, 1280}, {2, 1, 20, 9, 3, 0, 960}};  // 2-deep, 8 / 6 quads
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 // table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3

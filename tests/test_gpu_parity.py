@@ -345,7 +345,7 @@ def test_invalid_arguments_fail_without_side_effects(ctx, dev):
 
 
 # ------------------------------------------------------------------ K1 launch configurations
-@pytest.mark.parametrize("cfg", list(range(66)))
+@pytest.mark.parametrize("cfg", list(range(68)))
 def test_every_k1_config_matches_oracle(dev, cfg, monkeypatch):
     """All K1 launch configurations (ring depth, CTAs/SM, warps, hue table,
     lane layout, producer scheme) give the oracle's histograms, incl. ragged
