@@ -573,7 +573,31 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const int32_t seg_now = it.seg, frame_now = it.frame;
     const bool last = (i + 1 == n);
     const bool changed = it.next(!last);
-    if (MODE != kModeRead && (last || changed)) {
+#ifdef CLIPDETECT_EXP_NO_FLUSH
+    // experiment build only (tools/): flush once at the end (wrong per-frame bins)
+    const bool flush_now = last;
+#else
+    const bool flush_now = last || changed;
+#endif
+#ifdef CLIPDETECT_EXP_FLUSH2
+    // experiment build only (tools/): codes straight to the frame's global bins
+    // (one RED per non-zero code, two barriers instead of three)
+    if (MODE != kModeRead && flush_now) {
+      named_bar_sync(1, kConsumers);
+      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
+      for (uint32_t c = tid; c < nentries; c += kConsumers) {
+        const uint32_t cnt = sm.hist[c];
+        if (cnt) {
+          sm.hist[c] = 0u;
+          atomicAdd(gh + (MODE == kModeFast ? sm.c2b[c] : c), cnt);
+        }
+      }
+      named_bar_sync(1, kConsumers);
+    }
+    if (false) {
+#else
+    if (MODE != kModeRead && flush_now) {
+#endif
       // flush the frame's partial histogram
       named_bar_sync(1, kConsumers);
       for (uint32_t c = tid; c < nentries; c += kConsumers) {

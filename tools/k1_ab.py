@@ -69,7 +69,10 @@ def main():
                 res[c].append(float("nan"))
     out = {f"cfg{c}": {"median_gbs": round(statistics.median(x), 1), "all": [round(y, 1) for y in x]}
            for c, x in res.items()}
-    print(json.dumps({"video": which, "frames": v.n, "bytes": frames.numel(), "sm_mhz_per_round": clocks, **out}))
+    import hashlib
+    sha = hashlib.sha256(ref.cpu().numpy().tobytes()).hexdigest()[:16]  # compare across library builds
+    print(json.dumps({"video": which, "frames": v.n, "bytes": frames.numel(), "sm_mhz_per_round": clocks,
+                      "lib": os.environ.get("CLIPDETECT_LIB", "default"), "hist_sha": sha, **out}))
 
 
 if __name__ == "__main__":
