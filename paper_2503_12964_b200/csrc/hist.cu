@@ -579,10 +579,11 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 #else
     const bool flush_now = last || changed;
 #endif
-#ifdef CLIPDETECT_EXP_FLUSH2
-    // experiment build only (tools/): codes straight to the frame's global bins
-    // (one RED per non-zero code, two barriers instead of three)
     if (MODE != kModeRead && flush_now) {
+      // flush the frame's partial code histogram straight to the frame's global
+      // bins: one RED per non-zero code, two barriers (the older two-level flush
+      // through a shared bin histogram took three; +0.2-0.8 % K1, identical bins,
+      // profiles/r01/flush/)
       named_bar_sync(1, kConsumers);
       uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
       for (uint32_t c = tid; c < nentries; c += kConsumers) {
@@ -590,30 +591,6 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
         if (cnt) {
           sm.hist[c] = 0u;
           atomicAdd(gh + (MODE == kModeFast ? sm.c2b[c] : c), cnt);
-        }
-      }
-      named_bar_sync(1, kConsumers);
-    }
-    if (false) {
-#else
-    if (MODE != kModeRead && flush_now) {
-#endif
-      // flush the frame's partial histogram
-      named_bar_sync(1, kConsumers);
-      for (uint32_t c = tid; c < nentries; c += kConsumers) {
-        const uint32_t cnt = sm.hist[c];
-        if (cnt) {
-          sm.hist[c] = 0u;
-          atomicAdd(&sm.binacc[MODE == kModeFast ? sm.c2b[c] : c], cnt);
-        }
-      }
-      named_bar_sync(1, kConsumers);
-      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
-      for (uint32_t bn = tid; bn < nbins; bn += kConsumers) {
-        const uint32_t sum = sm.binacc[bn];
-        if (sum) {
-          sm.binacc[bn] = 0u;
-          atomicAdd(gh + bn, sum);
         }
       }
       named_bar_sync(1, kConsumers);

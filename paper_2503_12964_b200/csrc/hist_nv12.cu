@@ -346,21 +346,14 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     const bool last = (i + 1 == n);
     const bool changed = it.next(!last);
     if (MODE == kModeFast && (last || changed)) {
+      // one RED per non-zero code to the frame's global bins (as K1)
       named_bar_sync(1, kNvConsumers);
+      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
       for (uint32_t cc = tid; cc < (uint32_t)kEntries; cc += kNvConsumers) {
         const uint32_t cnt = sm.hist[cc];
         if (cnt) {
           sm.hist[cc] = 0u;
-          atomicAdd(&sm.binacc[sm.c2b[cc]], cnt);
-        }
-      }
-      named_bar_sync(1, kNvConsumers);
-      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
-      for (uint32_t bn = tid; bn < nbins; bn += kNvConsumers) {
-        const uint32_t sum = sm.binacc[bn];
-        if (sum) {
-          sm.binacc[bn] = 0u;
-          atomicAdd(gh + bn, sum);
+          atomicAdd(gh + sm.c2b[cc], cnt);
         }
       }
       named_bar_sync(1, kNvConsumers);
