@@ -17,9 +17,9 @@
 //    a 64 KiB hue table); the code of each lane is the byte offset of its
 //    entry in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm]
 //    -> ATOMS.POPC.INC, same-address lanes combined in hardware);
-//  * at a frame change the code histogram is mapped to the 162 bins
-//    (code_to_bin_dir, an 8 KB smem table) and added to the global u32
-//    histogram (integer adds: order-free, bit-deterministic).
+//  * at a frame change each non-zero code count is added to its bin of the
+//    frame's global u32 histogram (code_to_bin_dir, an 8 KB smem table; one
+//    RED per code; integer adds: order-free, bit-deterministic).
 // Older code layouts (cfg0-21: threshold codes, LUT codes) stay selectable
 // for tuning (CLIPDETECT_K1_CFG) and are parity-tested like the default.
 #include <stddef.h>
@@ -108,7 +108,7 @@ struct K1Smem {
   alignas(128) uint8_t buf[STAGES][SG * 48];
   uint8_t lut[LUT ? kLutBytes : 16];
   uint32_t hist[kEntries];  // CTA-shared code (or bin) histogram
-  uint32_t binacc[256];     // flush: per-bin sums
+  uint32_t binacc[256];     // unused since the two-barrier flush (kept: layout of the tuned configs)
   uint8_t c2b[kEntries];    // code -> bin
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
