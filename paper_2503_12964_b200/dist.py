@@ -97,7 +97,7 @@ def frame_shards(n: int, world: int) -> list:
 
 
 def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_all=None,
-                      marks=None):
+                      marks=None, comm=None, out=None):
     """One long video split by frame ranges across the ranks of `group`
     (the context-parallel analogue on the frame axis).
 
@@ -115,9 +115,15 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     `emb`: f32 cuda [m, D].
     `marks`: optional list; CUDA events recorded after each phase are appended
     (diagnosis of the exchange overhead).
+    `comm`: the collective provider (default torch.distributed; the GPU tests
+    pass an in-process one so that several virtual ranks share one GPU).
+    `out`: optional dict; receives this shard's histograms ("hist") and the
+    whole video's L1 ("l1").
     Returns (detected list, final list, cos tensor, band hits, rounds)."""
     import torch
-    import torch.distributed as dist
+    if comm is None:
+        import torch.distributed as comm
+    dist = comm
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     nv12 = frames.dim() == 3  # NV12 surfaces [m, H*3/2, W] (NEXT f1)
@@ -175,4 +181,6 @@ def run_video_sharded(ctx, frames, emb, n_total: int, f0: int, group=None, emb_a
     mark()
     merged, cos, hits, rounds = ctx.merge(emb_all, cuts[:max(1, n_cuts)].contiguous(), n_cuts=n_cuts)
     mark()
+    if out is not None:
+        out["hist"], out["l1"] = hist, l1_full
     return (cuts[:n_cuts].cpu().tolist(), merged.cpu().tolist(), cos, hits, rounds)
