@@ -26,8 +26,7 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Each source compiled to an object in parallel (hist.cu, with every K1
-    launch configuration, dominates), then one shared-library link."""
+    """Each source compiled to an object in parallel, then one shared-library link."""
     if force or stale():
         from concurrent.futures import ThreadPoolExecutor
 
@@ -37,21 +36,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             cflags = ["-Xptxas=-v"] + cflags
 
-        def compile_one(job):
-            src, defs = job
-            tag = "".join(d.split("=")[-1] for d in defs if d.startswith("-DK1_TU"))
-            obj = os.path.join(objdir, os.path.splitext(src)[0] + tag + ".o")
-            subprocess.check_call(["nvcc", *cflags, *defs, "-c", "-o", obj,
-                                   os.path.join(CSRC, src)], cwd=CSRC)
+        def compile_one(src):
+            obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+            subprocess.check_call(["nvcc", *cflags, "-c", "-o", obj, os.path.join(CSRC, src)],
+                                  cwd=CSRC)
             return obj
 
-        # hist.cu once per K1 mode (its every-configuration instantiations dominate)
-        # (the per-mode TUs leave some configuration helpers unused: warning 177)
-        jobs = [(s, ["-diag-suppress=177", f"-DK1_TU={t}"]) for s in SOURCES if s == "hist.cu"
-                for t in range(3)]
-        jobs += [(s, []) for s in SOURCES if s != "hist.cu"]
-        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
-            objs = list(ex.map(compile_one, jobs))
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            objs = list(ex.map(compile_one, SOURCES))
         subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                                "-Xcompiler", "-fPIC", "-o", LIB, *objs], cwd=CSRC)
     return LIB

@@ -87,7 +87,7 @@ def load(build_if_missing: bool = False):
     global _lib
     if _lib is not None:
         return _lib
-    path = os.environ.get("CLIPDETECT_LIB", LIB_PATH)  # experiment builds (tools/) only
+    path = LIB_PATH
     if not os.path.exists(path):
         if build_if_missing:
             _build.build()

@@ -37,8 +37,6 @@ struct clip_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   int sm_count = kSMs;
-  int nv12_dir = 6;  // K1-NV12 code layout: 0 = LUT codes, 1-7 = direct offsets (hist_nv12.cu; CLIPDETECT_NV12_DIR)
-  int k1_cfg = 55;  // K1 launch configuration: direct-offset codes, (d ^ na) bank hash, 3 x 37.5 KiB ring, 20 consumer warps (CLIPDETECT_K1_CFG overrides)
   bool sticky = false;
   std::string err;
   clip_stats stats{};
@@ -186,16 +184,11 @@ int k1_mode(const clip_params& p) {
   return (p.h_bins == 18 && p.s_bins == 3 && p.v_bins == 3) ? kModeFast : kModeGeneric;
 }
 
-int64_t stages_of(int64_t groups, int cfg) {
-  const int64_t sg = k1_stage_groups(cfg);
-  return (groups + sg - 1) / sg;
-}
-
 // One K1 launch over a list of segments (hist pointers already set).
 int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   int64_t total = 0;
   for (auto& s : segs) {
-    s.stages = stages_of(s.groups, ctx->k1_cfg);
+    s.stages = k1_stages(s.groups);
     s.stage_base = total;
     total += s.n_frames * s.stages;
   }
@@ -204,11 +197,9 @@ int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   CK(cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(HistSeg),
                      cudaMemcpyHostToDevice, ctx->stream));
   CKS(ensure(ctx, ctx->sink, 16));
-  const int grid = k1_grid(ctx->k1_cfg, ctx->sm_count, total);
   Span sp(ctx, 0);
-  CK(k1_launch(mode, ctx->k1_cfg, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total,
-               ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), grid,
-               ctx->stream));
+  CK(k1_launch(mode, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total, ctx->p.h_bins,
+               ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count, ctx->stream));
   sp.end();
   ctx->stats.k1_launches += 1;
   ctx->stats.launches += 1;
@@ -244,7 +235,7 @@ int launch_k1_nv12(clip_ctx* ctx, const std::vector<Nv12Seg>& all, int mode) {
     Span sp(ctx, 0);
     CK(k1_nv12_launch(k ? kModeGeneric : mode, P<Nv12Seg>(db), (int32_t)segs.size(), total,
                       p.h_bins, p.s_bins, p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count,
-                      ctx->nv12_dir, ctx->stream));
+                      ctx->stream));
     sp.end();
     ctx->stats.k1_launches += 1;
     ctx->stats.launches += 1;
@@ -449,14 +440,6 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
   ctx->device = cuda_device;
   ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   ctx->sm_count = prop.multiProcessorCount;
-  if (const char* e = getenv("CLIPDETECT_K1_CFG")) {
-    const int c = atoi(e);
-    if (c >= 0 && c < k1_num_cfgs()) ctx->k1_cfg = c;
-  }
-  if (const char* e = getenv("CLIPDETECT_NV12_DIR")) {
-    const int c = atoi(e);
-    if (c >= 0 && c <= 7) ctx->nv12_dir = c;
-  }
   if (cudaSetDevice(cuda_device) != cudaSuccess || k1_configure() != cudaSuccess ||
       k1_nv12_configure() != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -926,7 +909,7 @@ int clip_debug_binmap(clip_ctx* ctx, uint8_t* table) {
   CKS(check_ctx(ctx));
   if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
   CK(k5_binmap_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
-                      k1_mode(ctx->p) == kModeFast, k1_cfg_uses_lut(ctx->k1_cfg), ctx->stream));
+                      k1_mode(ctx->p) == kModeFast, ctx->stream));
   ctx->stats.launches += 1;
   return CLIP_OK;
 }
@@ -975,7 +958,7 @@ int clip_debug_nv12map(clip_ctx* ctx, uint8_t* table) {
   CKS(check_ctx(ctx));
   if (!table) return fail(ctx, CLIP_E_INVALID, "table is NULL");
   CK(k5_nv12map_launch(table, ctx->p.h_bins, ctx->p.s_bins, ctx->p.v_bins,
-                       k1_mode(ctx->p) == kModeFast, ctx->nv12_dir, ctx->stream));
+                       k1_mode(ctx->p) == kModeFast, ctx->stream));
   ctx->stats.launches += 1;
   return CLIP_OK;
 }

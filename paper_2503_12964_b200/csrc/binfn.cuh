@@ -8,15 +8,16 @@
 // channels, sector k in 0..5 (60 degrees each), in-sector numerator
 //   num = mid - min (k even, hue rising)   or   max - mid (k odd, falling),
 // so that the exact hue numerator is num6 = k*d + num over 6d (d = max - min),
-// and for nh = 18: h = 3k + floor(3*num/d), an integer threshold count.
+// and for nh = 18: h = 3k + floor(3*num/d).
 //
 // Hot path (18, 3, 3): TWO pixels per 32-bit register (u16x2 lanes).  Every
-// threshold test a >= b is the bit j of (a - b + 2^j) in its lane (no lane
-// borrows because |a - b| < 2^j <= 2^15), and the tests are OR-ed into a
-// per-lane 11-bit CODE (bits 5..15 of the lane).  The histogram is kept over
-// codes; codes are mapped to the 162 bins (code_to_bin) only when a frame is
-// flushed.  Verified bit-exact against the oracle on all 2^24 colours, in both
-// lanes (tests/test_binfn_host.py on the CPU, K5 on the GPU).
+// threshold test a >= b is bit j of (a - b + 2^j) in its lane (no lane
+// borrows: |a - b| < 2^j <= 2^15).  The in-sector hue offsets come from a
+// 64 KiB shared-memory table indexed by (d, na = mid - min), and each lane's
+// code IS the byte offset of its entry in an 8192-entry code histogram (the
+// "direct-offset" layout below); codes are mapped to the 162 bins only when a
+// frame is flushed.  Verified bit-exact against the oracle on all 2^24
+// colours in both lanes (tests/test_binfn_host.py on the CPU, K5 on the GPU).
 #pragma once
 
 #include <stdint.h>
@@ -84,38 +85,15 @@ CD_HD uint32_t cd_min3_u16x2(uint32_t a, uint32_t b, uint32_t c) {
 #endif
 }
 
-CD_HD uint32_t cd_max_u16x2(uint32_t a, uint32_t b) {
-#if defined(__CUDA_ARCH__)
-  return __vmaxu2(a, b);
-#else
-  return cd_max3_u16x2(a, b, b);
-#endif
-}
-
-// ------------------------------------------------------------ code layout
-// Per 16-bit lane (one pixel):
-//   bit 5  A  = [r >= g]                 bit 11 q2 = [3num >= 2 d1]
-//   bit 6-7 v = floor(3 max / 256)       bit 12 s1 = [3d >= mx1]
-//   bit 8  q3 = [num >= d1]              bit 13 s2 = [3d >= 2 mx1]
-//   bit 9  B  = [g >= b]                 bit 14 0
-//   bit 10 q1 = [3num >= d1]             bit 15 ris = rising sector (k even)
-// d1 = max(d, 1), mx1 = max(max, 1).  Index into the code histogram: lane >> 5.
-constexpr int kCodeShift = 5;
-constexpr int kCodes = 1 << (16 - kCodeShift);  // 2048
-
-// Runtime multiplier constants.  Passed in as kernel arguments so that ptxas
-// cannot fold them and must issue IMAD / IMAD.HI: that arithmetic then runs on
-// the FMA pipe and leaves the ALU pipe (LOP3/PRMT/VIMNMX/SHF, the binding
-// pipe on sm_100) to the bit work.
+// Runtime multiplier constants.  Passed in as kernel arguments (and read back
+// through shared memory) so that ptxas cannot fold them and must issue IMAD:
+// that arithmetic then runs on the FMA pipe and leaves the ALU pipe
+// (LOP3/PRMT/VIMNMX/IADD3, the binding pipe on sm_100: DESIGN.md §7) to the
+// bit work.
 struct MadK {
-  uint32_t one, neg1, neg2, three;
-  uint32_t sl4;   // 2^4
-  uint32_t sl16;  // 2^16
-  uint32_t sl20;  // 2^20
-  uint32_t four, neg4, neg6, neg7, neg3;
+  uint32_t one, neg1, three, four, neg4, neg6;
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 0xFFFFFFFEu, 3u, 1u << 4, 1u << 16, 1u << 20,
-                     4u, 0xFFFFFFFCu, 0xFFFFFFFAu, 0xFFFFFFF9u, 0xFFFFFFFDu};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 3u, 4u, 0xFFFFFFFCu, 0xFFFFFFFAu};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -125,185 +103,6 @@ CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #else
   return a * b + c;
 #endif
-}
-
-
-// Two pixels: R, G, B hold (channel of pixel 0) | (channel of pixel 1) << 16.
-// Every lane result below stays in [0, 2^16): no borrow or carry crosses lanes.
-CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B, MadK k) {
-  constexpr uint32_t kB15 = 0x80008000u;
-  const uint32_t mx = cd_max3_u16x2(R, G, B);
-  const uint32_t mn = cd_min3_u16x2(R, G, B);
-  const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t mid = R + G + B - mx - mn;     // two IADD3 (ALU)
-  const uint32_t na = cd_mad(mn, k.neg1, mid);  // rising numerator  mid - min
-  const uint32_t nb = cd_mad(mid, k.neg1, mx);  // falling numerator max - mid
-  const uint32_t R15 = cd_mad(R, k.one, kB15);
-  const uint32_t tA = cd_mad(G, k.neg1, R15);                     // bit 15: r >= g
-  const uint32_t tB = cd_mad(B, k.neg1, cd_mad(G, k.one, kB15));  // bit 15: g >= b
-  const uint32_t tC = cd_mad(B, k.neg1, R15);                     // bit 15: r >= b
-  const uint32_t ris = tA ^ tB ^ tC;              // bit 15: odd #(>=) <=> rising sector
-  const uint32_t pm = cd_prmt(ris, 0u, 0xBB99u);  // lane mask 0xFFFF if rising
-  const uint32_t num = (nb & ~pm) | (na & pm);
-  const uint32_t d1 = cd_max_u16x2(d, 0x00010001u);
-  const uint32_t mx1 = cd_max_u16x2(mx, 0x00010001u);
-  const uint32_t q1 = cd_mad(num, k.three, cd_mad(d1, k.neg1, 0x04000400u));  // 3num - d1 + 2^10
-  const uint32_t q2 = cd_mad(num, k.three, cd_mad(d1, k.neg2, 0x08000800u));  // 3num - 2d1 + 2^11
-  const uint32_t q3 = cd_mad(d1, k.neg1, cd_mad(num, k.one, 0x01000100u));   // num - d1 + 2^8
-  const uint32_t s1 = cd_mad(d, k.three, cd_mad(mx1, k.neg1, 0x10001000u));  // 3d - mx1 + 2^12
-  const uint32_t s2 = cd_mad(d, k.three, cd_mad(mx1, k.neg2, 0x20002000u));  // 3d - 2mx1 + 2^13
-  const uint32_t vv = cd_mad(mx, k.three, 0u) >> 2;  // bits 8,9 of 3 max -> 6,7
-  const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
-  return (ab & 0x02200220u) | (vv & 0x00C000C0u) | (q3 & 0x01000100u) | (q1 & 0x04000400u) |
-         (q2 & 0x08000800u) | (s1 & 0x10001000u) | (s2 & 0x20002000u) | (ris & 0x80008000u);
-}
-
-CD_HD uint32_t code_pair(uint32_t R, uint32_t G, uint32_t B) { return code_pair(R, G, B, kMadK); }
-
-// Byte offsets (4 * code index) of the two lanes' histogram entries.  Plain
-// shifts: IMAD.HI runs at a quarter of the IMAD rate on sm_100 (measured,
-// tools/isa_micro.cu), SHF at the ALU rate; lane 0 goes through IMAD (x << 16).
-CD_HD uint32_t code_off_lo(uint32_t code, MadK k) { return cd_mad(code, k.sl16, 0u) >> 19; }
-CD_HD uint32_t code_off_hi(uint32_t code, MadK k) { return code >> 19; }
-
-// code index (lane >> 5) -> bin in [0,162), or 255 for an unreachable code.
-CD_HD uint32_t code_to_bin(uint32_t idx) {
-  const uint32_t c = idx << kCodeShift;
-  const uint32_t A = (c >> 5) & 1u, v = (c >> 6) & 3u, q3 = (c >> 8) & 1u, B = (c >> 9) & 1u;
-  const uint32_t q1 = (c >> 10) & 1u, q2 = (c >> 11) & 1u, s1 = (c >> 12) & 1u;
-  const uint32_t s2 = (c >> 13) & 1u, z = (c >> 14) & 1u, ris = (c >> 15) & 1u;
-  const uint32_t C = A ^ B ^ ris;  // ris = A ^ B ^ C
-  const uint32_t oidx = (A << 2) | (B << 1) | C;
-  if (z || oidx == 1u || oidx == 6u || v > 2u) return 255u;
-  const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
-  return (k3 + q1 + q2 + q3) * 9u + (s1 + s2) * 3u + v;
-}
-
-// ------------------------------------------------------------ LUT variant
-// The in-sector hue offsets come from a 64 KiB shared-memory table instead of
-// three threshold tests and a select:
-//   lut[d*256 + (na ^ d)] = qr | qf << 2,
-//   qr = floor(3 na / d) (rising sectors), qf = floor(3 (d - na) / d) (falling),
-// na = mid - min, d = max - min (entry 0 for grey).  The XOR spreads lanes
-// with equal na over the 32 banks.  Lane code layout (index = lane >> 3):
-//   bit 3 A, bits 4-7 q (qr | qf << 2), bits 8-9 v, bit 10 s1 = [3d >= max],
-//   bit 11 s2 = [3d >= 2 max], bit 12 B, bits 13-14 0, bit 15 C  -> 5120 code indices.
-constexpr int kLutCodeShift = 3;
-constexpr int kLutCodes = 5120;
-
-CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
-  if (d == 0) return 0u;
-  const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
-  return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
-}
-// Bank swizzles of the table (the bank of entry (d, na) is bits 2-6 of the
-// byte index): 0 none; 1 na ^ d; 2 na ^ ((d << 2) & 0xFC), i.e. bank =
-// (d ^ (na >> 2)) & 31 — rows d and d+1 land in different banks, which keeps
-// the lookups of a warp on smooth content (d, na jittering by +-1 around a few
-// values, e.g. decoded NV12 where the luma noise moves r, g, b together)
-// nearly conflict-free (bank-conflict simulation in DESIGN.md §7).
-// 3: (na + 4d) mod 256 — the same bank spread as 2 (bank = (na/4 + d) mod 32,
-// up to a carry) but computed by one IMAD on the FMA pipe instead of a LOP3 on
-// the busier ALU pipe (the mod 256 is free: the index PRMT takes the low byte).
-CD_HD uint32_t lut_swizzle(uint32_t d, int swz) {
-  return swz == 2 ? ((d << 2) & 0xFCu) : (swz == 1 ? d : 0u);
-}
-CD_HD uint32_t lut_index(uint32_t na, uint32_t d, int swz = 3) {
-  return d * 256u + (swz == 3 ? ((na + 4u * d) & 255u) : (na ^ lut_swizzle(d, swz)));
-}
-// inverse: the na stored at byte b of row d
-CD_HD uint32_t lut_unswizzle(uint32_t b, uint32_t d, int swz) {
-  return swz == 3 ? ((b - 4u * d) & 255u) : (b ^ lut_swizzle(d, swz));
-}
-
-// Part 1 (before the table lookups): returns the partial code and the two
-// lanes' table indices.  The sector is carried as the three raw ordering
-// flags A, B, C (parity is decoded from them in code_to_bin_lut).
-template <int SWZ = 3>
-CD_HD uint32_t code_pair_lut_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
-                                 uint32_t& i1) {
-  constexpr uint32_t kB15 = 0x80008000u;
-  const uint32_t mx = cd_max3_u16x2(R, G, B);
-  const uint32_t mn = cd_min3_u16x2(R, G, B);
-  const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t sum = cd_mad(B, k.one, cd_mad(R, k.one, G));
-  const uint32_t na = cd_mad(mn, k.neg2, cd_mad(mx, k.neg1, sum));  // mid - min
-  // bank swizzle (lut_swizzle, both lanes at once)
-  const uint32_t nas = SWZ == 3 ? cd_mad(d, 4u, na)  // lanes stay < 2^16: no carry between them
-                       : SWZ == 2 ? (na ^ (cd_mad(d, 4u, 0u) & 0x00FC00FCu)) : (SWZ == 1 ? (na ^ d) : na);
-  i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8 (bytes 2-3 from d: zero)
-  i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
-  const uint32_t R15 = cd_mad(R, k.one, kB15);
-  const uint32_t tA = cd_mad(G, k.neg1, R15);  // bit 15: r >= g   (IMAD)
-  const uint32_t tB = G + kB15 - B;            // bit 15: g >= b   (IADD3)
-  const uint32_t tC = cd_mad(B, k.neg1, R15);  // bit 15: r >= b   (IMAD)
-  // s flags against max itself: black (max = 0) sets both, but a grey pixel is
-  // recognisable from its table entry (qr = qf = 0 only when d = 0) and
-  // code_to_bin_lut forces s = 0 for it.
-  const uint32_t z1 = cd_mad(mx, k.neg1, 0x04000400u);
-  const uint32_t s1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10
-  const uint32_t s2 = cd_mad(z1, k.one, s1);   // 3d - 2mx + 2^11
-  const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8,9 of 3 max = v
-  const uint32_t ab = cd_prmt(tA, tB, 0xFBD9u);  // byte0 = A mask, byte1 = B mask
-  return (ab & 0x10081008u) | (m3 & 0x03000300u) | (s1 & 0x04000400u) | (s2 & 0x08000800u) |
-         (tC & 0x80008000u);
-}
-// Part 2: add the two looked-up entries (q0 for lane 0, q1 for lane 1).
-CD_HD uint32_t code_pair_lut_post(uint32_t pre, uint32_t q0, uint32_t q1, MadK k) {
-  return cd_mad(q1, k.sl20, cd_mad(q0, k.sl4, pre));
-}
-// Byte offsets (4 * code index) of the two lanes' entries.
-CD_HD uint32_t lut_off_lo(uint32_t code, MadK k) { return cd_mad(code, k.sl16, 0u) >> 17; }
-CD_HD uint32_t lut_off_hi(uint32_t code, MadK k) { return code >> 17; }
-
-CD_HD uint32_t code_to_bin_lut(uint32_t idx) {
-  const uint32_t c = idx << kLutCodeShift;
-  const uint32_t A = (c >> 3) & 1u, qr = (c >> 4) & 3u, qf = (c >> 6) & 3u, v = (c >> 8) & 3u;
-  const uint32_t s1 = (c >> 10) & 1u, s2 = (c >> 11) & 1u, B = (c >> 12) & 1u;
-  const uint32_t z = (c >> 13) & 3u, C = (c >> 15) & 1u;
-  const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
-  const uint32_t oidx = (A << 2) | (B << 1) | C;
-  if (z || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
-  if (qr == 0u && qf == 0u) return oidx == 7u ? v : 255u;  // grey (d = 0): h = 0, s = 0
-  const uint32_t k3 = (kSector3k >> (oidx << 2)) & 15u;
-  return (k3 + (ris ? qr : qf)) * 9u + (s1 + s2) * 3u + v;
-}
-
-// ------------------------------------------------------------ direct-offset variant
-// Each lane's code IS the byte offset of its code-histogram entry, so nothing
-// runs between the table lookup and the shared-memory atomic but one PRMT:
-//   offset = byte1 << 8 | byte0,
-//   byte0 = the table entry: q3 << 2 | hash << 5  (bits 0-1 zero),
-//   byte1 = v (bits 8-9) | s1 (10) | s2 (11) | A = [r>=g] (12) | B = [g>=b] (13)
-//           | C = [r>=b] (14) | 0 (15)          -> offsets < 0x8000: 8192 entries.
-// q3 in [0, 8) is the compact index of the table's (qr, qf) pair (kDirQ below);
-// hash (2 bits, a function of (d, na) that the bin ignores) only spreads the
-// entries over the 32 shared-memory banks: the bank of an entry is offset bits
-// 2-6 = (q3, hash), all from byte 0.  Without it a warp's atomics on noisy
-// content would share 8 banks.
-// The byte-1 fields are threshold bits (a - b + 2^j, see code_pair) merged by
-// bit-selects: every select takes ONE field from its source and keeps the rest,
-// and the field values never carry into bit 15.  The table index is the
-// swizzle-3 index (na + 4d) mod 256, computed straight from the channel sum:
-//   na + 4d = (r + g + b) + 3 max - 6 min   (mid = sum - max - min).
-constexpr int kDirCodes = 8192;
-// (qr, qf) of q3 = 0..7: grey, then na/d = 0, (0,1/3), 1/3, (1/3,2/3), 2/3, (2/3,1), 1
-constexpr uint32_t kDirQ = (0u << 0) | (12u << 4) | (8u << 8) | (9u << 12) | (5u << 16) |
-                           (6u << 20) | (2u << 24) | (3u << 28);  // nibble = qr | qf << 2
-CD_HD uint32_t dir_q3(uint32_t q) {  // (qr | qf << 2) -> q3
-  for (uint32_t i = 0; i < 8; ++i)
-    if (((kDirQ >> (4 * i)) & 15u) == q) return i;
-  return 0u;
-}
-// hash modes: 0 none, 1 d & 3, 2 na & 3, 3 (d ^ na) & 3, 4 ((d >> 5) ^ na) & 3,
-// 5 ((d >> 6) ^ d) & 3
-CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d, int hash = 1) {
-  const uint32_t h = hash == 1 ? d
-                     : hash == 2 ? na
-                     : hash == 3 ? (d ^ na)
-                     : hash == 4 ? ((d >> 5) ^ na)
-                     : hash == 5 ? ((d >> 6) ^ d) : 0u;
-  return (dir_q3(lut_entry(na, d)) << 2) | ((h & 3u) << 5);
 }
 
 // bit select (a where m, else b) as ONE LOP3: written as inline PTX so that the
@@ -319,38 +118,77 @@ CD_HD uint32_t cd_sel(uint32_t a, uint32_t b) {
 #endif
 }
 
-// Table index with swizzle multiplier KS: byte (na + KS d) mod 256 of row d.
-CD_HD uint32_t lut_index_k(uint32_t na, uint32_t d, uint32_t ks) { return d * 256u + ((na + ks * d) & 255u); }
-CD_HD uint32_t lut_unswizzle_k(uint32_t b, uint32_t d, uint32_t ks) { return (b - ks * d) & 255u; }
+// ------------------------------------------------------------ hue table
+// lut_entry: qr | qf << 2 with qr = floor(3 na / d) (rising sectors) and
+// qf = floor(3 (d - na) / d) (falling), both clamped to 3; 0 for grey (d = 0).
+CD_HD uint32_t lut_entry(uint32_t na, uint32_t d) {
+  if (d == 0) return 0u;
+  const uint32_t qr = (3u * na) / d, qf = (3u * (d - na)) / d;
+  return (qr > 3u ? 3u : qr) | ((qf > 3u ? 3u : qf) << 2);
+}
+
+// Table row d holds na at byte (na + 4d) mod 256: rows d and d + 1 of the same
+// na land in different banks (the swizzle keeps warps on smooth content, where
+// (d, na) jitter by +-1, nearly conflict-free), and the index comes straight
+// from the channel sum (code_pair_dir_pre).
+CD_HD uint32_t lut_index(uint32_t na, uint32_t d) { return d * 256u + ((na + 4u * d) & 255u); }
+CD_HD uint32_t lut_unswizzle(uint32_t b, uint32_t d) { return (b - 4u * d) & 255u; }
+
+// ------------------------------------------------------------ direct-offset codes
+// Each lane's code IS the byte offset of its code-histogram entry, so nothing
+// runs between the table lookup and the shared-memory atomic but one PRMT:
+//   offset = byte1 << 8 | byte0,
+//   byte0 = the table entry: q3 << 2 | hash << 5  (bits 0-1 zero),
+//   byte1 = v (bits 8-9) | s1 (10) | s2 (11) | A = [r>=g] (12) | B = [g>=b] (13)
+//           | C = [r>=b] (14) | 0 (15)          -> offsets < 0x8000: 8192 entries.
+// q3 in [0, 8) is the compact index of the table's (qr, qf) pair (kDirQ below);
+// hash (2 bits, a function of (d, na) that the bin ignores) only spreads the
+// entries over the 32 shared-memory banks: the bank of an entry is offset bits
+// 2-6 = (q3, hash), all from byte 0.  Without it a warp's atomics on noisy
+// content would share 8 banks.
+constexpr int kDirCodes = 8192;
+// (qr, qf) of q3 = 0..7: grey, then na/d = 0, (0,1/3), 1/3, (1/3,2/3), 2/3, (2/3,1), 1
+constexpr uint32_t kDirQ = (0u << 0) | (12u << 4) | (8u << 8) | (9u << 12) | (5u << 16) |
+                           (6u << 20) | (2u << 24) | (3u << 28);  // nibble = qr | qf << 2
+CD_HD uint32_t dir_q3(uint32_t q) {  // (qr | qf << 2) -> q3
+  for (uint32_t i = 0; i < 8; ++i)
+    if (((kDirQ >> (4 * i)) & 15u) == q) return i;
+  return 0u;
+}
+// Bank hashes (tools/atoms_bank_sim.py): K1 (RGB24) uses (d ^ na) & 3, K1-NV12
+// ((d >> 5) ^ na) & 3 — on decoded NV12 the luma noise moves r, g, b
+// together, so d is nearly constant within a palette cell.
+enum { kHashRgb = 0, kHashNv12 = 1 };
+CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d, int hash) {
+  const uint32_t h = hash == kHashNv12 ? ((d >> 5) ^ na) : (d ^ na);
+  return (dir_q3(lut_entry(na, d)) << 2) | ((h & 3u) << 5);
+}
 
 // Part 1: byte 1 of both lanes' offsets (in bytes 1 and 3 of the result) and
-// the two table indices.  TBF = 1 computes B (2: A and B) on the FMA pipe (two
-// IMADs each) instead of one IADD3 each on the ALU pipe.  KS = table swizzle multiplier (4 or 5):
-// na + KS d = sum + (KS - 1) max - (KS + 2) min.
-// XU = 1: the lanes carry a per-pixel offset 256 X in their high byte (the same
-// X for the pixel's three channels, unpack4x): orderings, differences, d and the
-// table index are unchanged; the two terms that need the absolute max take the
-// offset back through their addends, kz = 2^10 + 256 X and km = -768 X.
-template <int TBF = 0, int KS = 4, int XU = 0>
+// the two table indices.  The table index is (na + 4d) mod 256 of row d,
+// computed straight from the channel sum: na + 4d = (r + g + b) + 3 max - 6 min
+// (mid = sum - max - min).  The byte-1 fields are threshold bits (a - b + 2^j)
+// merged by bit-selects: every select takes ONE field from its source and
+// keeps the rest, and the field values never carry into bit 15.
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
-                                 uint32_t& i1, uint32_t kz = 0u, uint32_t km = 0u) {
-  static_assert(KS == 4 || KS == 5, "swizzle multiplier");
+                                 uint32_t& i1) {
   const uint32_t mx = cd_max3_u16x2(R, G, B);
   const uint32_t mn = cd_min3_u16x2(R, G, B);
   const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, KS == 4 ? k.three : k.four, R)));
-  const uint32_t nas = cd_mad(mn, KS == 4 ? k.neg6 : k.neg7, t);  // na + KS d; lanes < 2^16
+  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, k.three, R)));
+  const uint32_t nas = cd_mad(mn, k.neg6, t);  // na + 4d; lanes < 2^16
   i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8
   i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
-  const uint32_t tA = TBF >= 2 ? cd_mad(G, k.neg1, cd_mad(R, k.one, 0x10001000u))
-                                : R + 0x10001000u - G;                 // bit 12: r >= g
-  const uint32_t tB = TBF ? cd_mad(B, k.neg1, cd_mad(G, k.one, 0x20002000u))
-                          : G + 0x20002000u - B;                       // bit 13: g >= b
+  const uint32_t tA = R + 0x10001000u - G;                                 // bit 12: r >= g
+  const uint32_t tB = G + 0x20002000u - B;                                 // bit 13: g >= b
   const uint32_t tC = cd_mad(B, k.neg4, cd_mad(R, k.four, 0x40004000u));  // bit 14: r >= b
-  const uint32_t z1 = cd_mad(mx, k.neg1, XU ? kz : 0x04000400u);
+  // s flags against max itself: black (max = 0) sets both, but a grey pixel is
+  // recognisable from its table entry (q3 = 0 only when d = 0) and
+  // code_to_bin_dir forces s = 0 for it.
+  const uint32_t z1 = cd_mad(mx, k.neg1, 0x04000400u);
   const uint32_t x1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10:  bit 10 = s1, < 2^11
   const uint32_t x2 = cd_mad(z1, k.one, x1);   // 3d - 2mx + 2^11: bit 11 = s2, < 2^12
-  const uint32_t m3 = cd_mad(mx, k.three, XU ? km : 0u);  // bits 8-9 of 3 max = v, < 2^10
+  const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8-9 of 3 max = v, < 2^10
   uint32_t p = cd_sel<0x04000400u>(x1, x2);  // bit 10 s1, bit 11 s2, bits 12-15 zero
   p = cd_sel<0x03000300u>(m3, p);
   p = cd_sel<0x10001000u>(tA, p);
@@ -425,7 +263,7 @@ CD_HD void nv12_pair_rgb(uint32_t ya, uint32_t yb, int32_t ruv, int32_t guv, int
 // Pack 4 pixels (12 bytes in words w0, w1, w2) into two u16x2 pairs:
 // (R01, G01, B01) = pixels 0,1 and (R23, G23, B23) = pixels 2,3.
 CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
-                   uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23, MadK k) {
+                   uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23) {
   // w0 = [r0 g0 b0 r1], w1 = [g1 b1 r2 g2], w2 = [b2 r3 g3 b3] (byte 0 first)
   const uint32_t s0 = w0 >> 8;  // [g0 b0 r1 0]
   const uint32_t s1 = w1 >> 8;  // [b1 r2 g2 0]
@@ -437,34 +275,8 @@ CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_
   B23 = cd_prmt(w2, 0u, 0x4340u);
 }
 
-CD_HD void unpack4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
-                   uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23) {
-  unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, kMadK);
-}
-
-// unpack4 without the two shifts: the high byte of every lane is a data byte X
-// of w1 (bytes 0 and 1: g1, b1), the same for the three channels of a pixel;
-// off = 256 X per lane for code_pair_dir_pre<.., XU = 1> (kz = off + 2^10, km = -3 off).
-CD_HD void unpack4x(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& R01, uint32_t& G01,
-                    uint32_t& B01, uint32_t& R23, uint32_t& G23, uint32_t& B23, uint32_t& off) {
-  // w0 = [r0 g0 b0 r1], w1 = [g1 b1 r2 g2], w2 = [b2 r3 g3 b3]; X0 = w1.b0, X1 = w1.b1
-  R01 = cd_prmt(w0, w1, 0x5340u);
-  G01 = cd_prmt(w0, w1, 0x5441u);
-  B01 = cd_prmt(w0, w1, 0x5542u);
-  R23 = cd_prmt(w1, w2, 0x1502u);
-  G23 = cd_prmt(w1, w2, 0x1603u);
-  B23 = cd_prmt(w1, w2, 0x1704u);
-  off = cd_prmt(w1, 0u, 0x1404u);
-}
-
-// -------------------------------------------------- scalar forms (reference/tests)
-// Fast scalar (18, 3, 3) form, same sector arithmetic, one pixel.
-CD_HD uint32_t bin_18_3_3(uint32_t r, uint32_t g, uint32_t b) {
-  const uint32_t c = code_pair(r, g, b) & 0xFFFFu;
-  return code_to_bin(c >> kCodeShift);
-}
-
-// General (nh, ns, nv) with nh*ns*nv <= 256 (integer division; not the hot path).
+// ------------------------------------------------- general layouts (not the hot path)
+// General (nh, ns, nv) with nh*ns*nv <= 256 (integer division).
 CD_HD uint32_t bin_generic(uint32_t r, uint32_t g, uint32_t b, uint32_t nh, uint32_t ns,
                            uint32_t nv) {
   uint32_t mx = r > g ? r : g;

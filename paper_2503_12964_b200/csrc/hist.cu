@@ -1,30 +1,34 @@
 // hist.cu — K1: fused RGB24 -> HSV bin -> per-frame histogram (rows a1-a3).
 //
-// hist_t[b] = #{pixels of frame t with bin b} (reading O2; §2.1).
+// hist_t[b] = #{pixels of frame t with bin b} (reading O2; §2.1
+// "analyzing the color changes between frames").
 //
-// B200 design (the default launch configuration is cfg55):
+// B200 design (DESIGN.md §7 "K1"):
 //  * persistent grid, one CTA per SM; each CTA owns a CONTIGUOUS range of
 //    "stages" of the flattened (segment, frame, stage) space, so a CTA flushes
 //    its histogram only when its frame changes;
-//  * one producer lane streams each stage (<= 800 x 48 B of one frame) HBM ->
-//    shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
-//    mbarrier::complete_tx, L2 evict_first) into a 3-deep ring; consumers
-//    signal "empty" per warp;
-//  * 20 consumer warps; each lane takes lane-contiguous 4-pixel quads (three
-//    conflict-free LDS.32), unpacks them into u16x2 pixel pairs and computes
-//    a per-pixel CODE two pixels per instruction (binfn.cuh
-//    code_pair_dir_pre: division-free sector form of the exact HSV bins with
-//    a 64 KiB hue table); the code of each lane is the byte offset of its
-//    entry in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm]
-//    -> ATOMS.POPC.INC, same-address lanes combined in hardware);
+//  * one producer lane streams each stage (<= 800 x 48 B = 37.5 KiB of one
+//    frame) HBM -> shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
+//    mbarrier::complete_tx, L2 evict_first) into a 3-deep mbarrier ring;
+//    consumer warps release a slot per warp ("empty" barrier);
+//  * 20 consumer warps; each lane takes 5 lane-contiguous 4-pixel quads of a
+//    stage (three conflict-free LDS.32 each, so one warp instruction covers
+//    128 adjacent pixels), unpacks them into u16x2 pixel pairs and computes a
+//    per-pixel CODE two pixels per instruction (binfn.cuh code_pair_dir_pre:
+//    division-free sector form of the exact HSV bins with a 64 KiB hue
+//    table), phase by phase over its 10 pixel pairs (loads, codes, table
+//    lookups, atomics); the code of each lane is the byte offset of its entry
+//    in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm] ->
+//    ATOMS.POPC.INC: same-address lanes combine in hardware);
 //  * at a frame change each non-zero code count is added to its bin of the
-//    frame's global u32 histogram (code_to_bin_dir, an 8 KB smem table; one
-//    RED per code; integer adds: order-free, bit-deterministic).
-// Older code layouts (cfg0-21: threshold codes, LUT codes) stay selectable
-// for tuning (CLIPDETECT_K1_CFG) and are parity-tested like the default.
+//    frame's global u32 histogram (code_to_bin_dir through an 8 KB smem table;
+//    one RED per code; integer adds: order-free, bit-deterministic).
+// 800-group stages split 720p, 1080p and 4K frames into whole stages (every
+// lane exactly 5 quads); other sizes end a frame with one ragged stage that
+// the lanes walk quad by quad.  Other bin layouts than 18x3x3 run the same
+// pipeline with the exact integer bin_generic per pixel (kModeGeneric); the
+// read-only variant (kModeRead, K6) measures the pipeline's HBM ceiling.
 #include <stddef.h>
-
-#include <utility>
 
 #include "binfn.cuh"
 #include "common.cuh"
@@ -34,90 +38,33 @@ namespace clipdetect {
 
 namespace {
 
-constexpr int kStageGroups = 512;  // default 48-byte groups per stage (24 KiB)
-constexpr uint32_t kDynSmemBase = 0x400;  // shared-window offset of dynamic smem (after 1 KiB system reserve)
+constexpr int kStages = 3;                     // TMA ring depth
+constexpr int kWarps = 20;                     // consumer warps
+constexpr int kConsumers = kWarps * 32;        // 640 consumer lanes
+constexpr int kThreads = kConsumers + 32;      // + one producer warp
+constexpr int kStageGroups = 800;              // 16-pixel (48-byte) groups per stage: 37.5 KiB
+constexpr int kQPL = 4 * kStageGroups / kConsumers;  // quads per lane in a full stage
+static_assert(kQPL * kConsumers == 4 * kStageGroups, "a full stage splits evenly over the lanes");
 constexpr int kLutBytes = 65536;
+// Shared-window address of dynamic shared memory: after the 1 KiB the system
+// reserves, for a launch without clusters (what ptxas itself assumes when it
+// materialises the base).  The kernel checks it at entry and falls back to
+// runtime addressing if it ever differs (k1_consume<MODE, false>).
+constexpr uint32_t kDynSmemBase = 0x400;
 
-// Launch configurations: ring depth, CTAs per SM, consumer warps, LUT hue.
-// quad = lane-contiguous layout: each lane takes 4 pixels (12 bytes, three
-// conflict-free LDS.32) so one warp instruction covers 128 adjacent pixels
-// (better same-address aggregation of the histogram atomics and of the hue
-// table lookups on spatially coherent content).
-// noprod = no dedicated producer warp: the last consumer warp to release a
-// ring slot issues the slot's next TMA copy (lets a CTA hold 32 consumer warps).
-struct K1Cfg {
-  int stages, ctas_per_sm, warps, lut, quad, noprod = 0, sg = kStageGroups;  // sg: groups per stage
-};
-constexpr K1Cfg kCfgs[] = {{4, 2, 8, 0, 0}, {2, 3, 8, 0, 0}, {3, 2, 8, 0, 0}, {6, 1, 8, 0, 0},
-                           {4, 1, 16, 1, 0}, {2, 1, 16, 1, 0}, {4, 1, 16, 0, 0},
-                           {4, 1, 16, 1, 1}, {4, 2, 8, 0, 1}, {4, 1, 16, 1, 2}, {4, 1, 8, 1, 2},
-                           {4, 2, 8, 0, 2}, {4, 1, 32, 1, 2, 1}, {4, 1, 16, 1, 2, 1},
-                           {4, 1, 16, 1, 3}, {4, 1, 16, 2, 2},  // lut 2 = table without swizzle
-                           {5, 1, 16, 1, 3}, {4, 1, 16, 3, 3},  // 5-deep ring; lut 3 = swizzle 2
-                           {3, 1, 16, 1, 3, 0, 768}, {2, 1, 16, 1, 3, 0, 1024},
-                           {4, 1, 16, 1, 3, 0, 640},  // larger stages: fewer ring hand-offs
-                           {4, 1, 16, 4, 3},   // lut 4 = swizzle 3 (IMAD instead of LOP3)
-                           {4, 1, 16, 5, 3}, {4, 1, 16, 6, 3},  // lut 5/6 = direct offsets
-                           {4, 1, 16, 5, 4},   // quad 4 = lane-contiguous octets (LDS.64)
-                           {4, 1, 8, 5, 3}, {3, 1, 16, 5, 3, 0, 768},  // fewer ring hand-offs per pixel
-                           {3, 1, 16, 5, 4, 0, 768},
-                           {4, 1, 16, 7, 3}, {4, 1, 16, 8, 3}, {4, 1, 16, 9, 3},  // bank hashes
-                           {4, 1, 16, 8, 4}, {4, 1, 16, 10, 3}, {4, 1, 16, 11, 3}, {4, 1, 16, 10, 4},
-                           {4, 1, 16, 12, 3}, {4, 1, 16, 12, 4},  // lut 12: swizzle multiplier 5
-                           {3, 1, 24, 10, 3, 0, 768}, {4, 1, 20, 10, 3, 0, 640},  // more warps
-                           {3, 1, 24, 12, 3, 0, 768}, {4, 1, 20, 12, 3, 0, 640},
-                           {4, 1, 32, 10, 3, 1}, {2, 1, 32, 10, 3, 1, 1024},  // 32 warps, no producer
-                           {4, 1, 16, 13, 3}, {4, 1, 16, 14, 3},  // lut 13/14: A, B on the FMA pipe
-                           {2, 1, 16, 10, 3, 0, 1024}, {2, 1, 32, 14, 3, 1, 1024},
-                           {3, 1, 16, 10, 3, 0, 768}, {4, 1, 16, 5, 3, 0, 640},  // 36 / 30 KiB stages
-                           {3, 1, 16, 9, 3, 0, 768}, {3, 1, 16, 6, 3, 0, 768},
-                           {4, 1, 16, 9, 3, 0, 640}, {3, 1, 16, 9, 4, 0, 768},
-                           {3, 1, 16, 15, 3, 0, 768}, {2, 1, 16, 9, 3, 0, 1024},  // lut 15: hash 3, swizzle 5
-                           {3, 1, 20, 9, 3, 0, 800},
-                           {3, 1, 16, 16, 3, 0, 768}, {3, 1, 16, 17, 3, 0, 768},  // unpack4x
-                           {3, 1, 20, 5, 3, 0, 800},   // d & 3 hash, 20 consumer warps
-                           {2, 1, 24, 9, 3, 0, 960}, {3, 1, 24, 9, 3, 0, 768},  // 24 consumer warps
-                           {4, 1, 20, 9, 5, 0, 640}, {3, 1, 20, 9, 5, 0, 640},  // quad 5: LDS.128 groups
-                           {2, 1, 20, 9, 5, 0, 1280}, {4, 1, 16, 9, 5, 0, 512},
-                           {4, 1, 20, 9, 3, 0, 640},   // 4-deep ring, 4 quads per lane
-                           {2, 1, 20, 9, 3, 0, 1280}, {2, 1, 20, 9, 3, 0, 960}};  // 2-deep, 8 / 6 quads
-constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
-
-// table swizzle of a config's hue table (binfn.cuh lut_swizzle): lut 1 -> 1, 2 -> 0, 3 -> 2, 4 -> 3
-__host__ __device__ constexpr int lut_swz(int lut) {
-  return lut == 1 ? 1 : (lut == 3 ? 2 : (lut >= 4 ? 3 : 0));
-}
-// lut 5-9: direct-offset codes (binfn.cuh code_pair_dir_pre; 6 = B on the FMA pipe),
-// bank hash of the table entries (binfn.cuh lut_entry_dir): 7 none, 8 na & 3,
-// 9 and 15 (d ^ na) & 3, 10, 12-14 ((d >> 5) ^ na) & 3, 11 ((d >> 6) ^ d) & 3, otherwise d & 3
-// (tools/atoms_bank_sim.py)
-__host__ __device__ constexpr bool lut_dir(int lut) { return lut >= 5; }
-__host__ __device__ constexpr int lut_hash(int lut) {
-  return lut == 7 ? 0 : (lut == 8 ? 2 : (lut == 9 || lut >= 15 ? 3 : (lut >= 10 && lut != 11 ? 4 : (lut == 11 ? 5 : 1))));
-}
-// table swizzle multiplier of the direct-offset configs: lut 12, 14 = 5, else 4
-__host__ __device__ constexpr int lut_ks(int lut) { return lut == 12 || lut == 14 || lut == 15 ? 5 : 4; }
-// unpack without shifts (unpack4x, code_pair_dir_pre XU): lut 16 (hash 3), 17 (hash 3, TBF 1)
-__host__ __device__ constexpr int lut_xu(int lut) { return lut == 16 || lut == 17 ? 1 : 0; }
-// flags A, B on the FMA pipe (code_pair_dir_pre TBF): lut 6, 17 -> B, lut 13, 14 -> A and B
-__host__ __device__ constexpr int lut_tbf(int lut) { return lut == 6 || lut == 17 ? 1 : (lut == 13 || lut == 14 ? 2 : 0); }
-
-template <int STAGES, int LUT, int SG>
 struct K1Smem {
-  static constexpr int kEntries = lut_dir(LUT) ? kDirCodes : (LUT ? kLutCodes : kCodes);
-  alignas(128) uint8_t buf[STAGES][SG * 48];
-  uint8_t lut[LUT ? kLutBytes : 16];
-  uint32_t hist[kEntries];  // CTA-shared code (or bin) histogram
-  uint32_t binacc[256];     // unused since the two-barrier flush (kept: layout of the tuned configs)
-  uint8_t c2b[kEntries];    // code -> bin
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint32_t cnt[STAGES];  // noprod: warps done with the slot's current stage
+  alignas(128) uint8_t buf[kStages][kStageGroups * 48];
+  uint8_t lut[kLutBytes];   // hue table: lut[lut_index(na, d)] = lut_entry_dir(na, d, kHashRgb)
+  uint32_t hist[kDirCodes];  // CTA-shared code histogram (bins for kModeGeneric)
+  uint8_t c2b[kDirCodes];    // code -> bin
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
   MadK mk;
 };
+constexpr uint32_t kLutOff = (uint32_t)offsetof(K1Smem, lut);
+constexpr uint32_t kHistOff = (uint32_t)offsetof(K1Smem, hist);
 
 // Walks the flattened (segment, frame, stage) space with 32-bit counters.
-template <int SG>
 struct StageIter {
   const HistSeg* segs;
   int32_t seg, frame, st;
@@ -130,7 +77,7 @@ struct StageIter {
     groups = g.groups;
     stages = (int32_t)g.stages;
     n_frames = (int32_t)g.n_frames;
-    last_ng = (int32_t)(g.groups - (g.stages - 1) * SG);
+    last_ng = (int32_t)(g.groups - (g.stages - 1) * kStageGroups);
     frames = g.frames;
   }
   __device__ void seek(const HistSeg* s, int32_t nseg, int64_t g) {
@@ -146,7 +93,10 @@ struct StageIter {
     frame = (int32_t)(rel / stages);
     st = (int32_t)(rel - (int64_t)frame * stages);
   }
-  __device__ __forceinline__ int32_t ng() const { return st == stages - 1 ? last_ng : SG; }
+  __device__ __forceinline__ int32_t ng() const { return st == stages - 1 ? last_ng : kStageGroups; }
+  __device__ __forceinline__ const uint8_t* src() const {
+    return frames + ((int64_t)frame * groups + (int64_t)st * kStageGroups) * 48;
+  }
   // advance; returns true if the frame (or segment) changed
   __device__ __forceinline__ bool next(bool more) {
     if (++st == stages) {
@@ -162,123 +112,33 @@ struct StageIter {
   }
 };
 
-#ifdef CLIPDETECT_EXP_NO_ATOMS
-// experiment build only (tools/): keep the codes alive without the histogram atomics
-__device__ uint32_t g_exp_sink;
-__device__ __forceinline__ void hist_inc(char* hb, uint32_t off) {
-  if (off == 0xFFFFFFFFu) g_exp_sink = off;
+// Shared-memory accesses of the hot loop at offset x of the hue table / the
+// code histogram.  IMM: the dynamic smem base is kDynSmemBase, so the address
+// is register + immediate (LDS / ATOMS [R + imm]: no per-access base add);
+// otherwise the runtime base `sb` is added.
+template <bool IMM>
+__device__ __forceinline__ uint32_t lut_ld(uint32_t sb, uint32_t x) {
+  uint32_t v;
+  if constexpr (IMM)
+    asm("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(x), "n"(kDynSmemBase + kLutOff));
+  else
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sb + kLutOff + x));
+  return v;
 }
-#else
-__device__ __forceinline__ void hist_inc(char* hb, uint32_t off) {
-  atomicAdd(reinterpret_cast<uint32_t*>(hb + off), 1u);
-}
-#endif
-// the same increment at a shared-window address given as register + constant
-// (ATOMS [R + imm]: no per-atomic base add)
-template <uint32_t BASE>
-__device__ __forceinline__ void hist_inc_s(uint32_t off) {
-#ifdef CLIPDETECT_EXP_NO_ATOMS
-  if (off == 0xFFFFFFFFu) g_exp_sink = off;
-#else
-  asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(off), "n"(BASE) : "memory");
-#endif
-}
-
-template <int MODE, int LUT>
-__device__ __forceinline__ void bin_group(const uint8_t* src, uint32_t* hist, const uint8_t* lut,
-                                          uint32_t nh, uint32_t ns, uint32_t nv, MadK mk,
-                                          uint32_t& xacc) {
-  const uint4* p = reinterpret_cast<const uint4*>(src);
-  const uint4 a = p[0], b = p[1], c = p[2];
-  const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-  if constexpr (MODE == kModeRead) {
-#pragma unroll
-    for (int i = 0; i < 12; ++i) xacc ^= w[i];
-    return;
-  } else if constexpr (MODE == kModeFast) {
-    char* hb = reinterpret_cast<char*>(hist);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t R01, G01, B01, R23, G23, B23;
-      unpack4(w[3 * q], w[3 * q + 1], w[3 * q + 2], R01, G01, B01, R23, G23, B23, mk);
-      uint32_t c01, c23;
-      if (LUT) {
-        uint32_t a0, a1, b0, b1;
-        const uint32_t p01 = code_pair_lut_pre<lut_swz(LUT)>(R01, G01, B01, mk, a0, a1);
-        const uint32_t p23 = code_pair_lut_pre<lut_swz(LUT)>(R23, G23, B23, mk, b0, b1);
-        c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
-        c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
-      } else {
-        c01 = code_pair(R01, G01, B01, mk);
-        c23 = code_pair(R23, G23, B23, mk);
-      }
-      // byte offsets of the code-histogram entries
-      if (LUT) {
-        hist_inc(hb, lut_off_lo(c01, mk));
-        hist_inc(hb, lut_off_hi(c01, mk));
-        hist_inc(hb, lut_off_lo(c23, mk));
-        hist_inc(hb, lut_off_hi(c23, mk));
-      } else {
-        hist_inc(hb, code_off_lo(c01, mk));
-        hist_inc(hb, code_off_hi(c01, mk));
-        hist_inc(hb, code_off_lo(c23, mk));
-        hist_inc(hb, code_off_hi(c23, mk));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int o = 3 * i;
-      const uint32_t r = __byte_perm(w[o >> 2], 0u, 0x4440u | (o & 3));
-      const uint32_t g = __byte_perm(w[(o + 1) >> 2], 0u, 0x4440u | ((o + 1) & 3));
-      const uint32_t bb = __byte_perm(w[(o + 2) >> 2], 0u, 0x4440u | ((o + 2) & 3));
-      atomicAdd(&hist[bin_generic(r, g, bb, nh, ns, nv)], 1u);
-    }
-  }
-}
-
-// 4 pixels (12 bytes at a 4-byte aligned smem address) -> 4 histogram increments
-template <int LUT>
-__device__ __forceinline__ void bin_quad(const uint8_t* src, uint32_t* hist, const uint8_t* lut,
-                                         MadK mk) {
-  const uint32_t* p = reinterpret_cast<const uint32_t*>(src);
-  const uint32_t w0 = p[0], w1 = p[1], w2 = p[2];
-  char* hb = reinterpret_cast<char*>(hist);
-  uint32_t R01, G01, B01, R23, G23, B23;
-  unpack4(w0, w1, w2, R01, G01, B01, R23, G23, B23, mk);
-  if constexpr (lut_dir(LUT)) {
-    uint32_t a0, a1, b0, b1;
-    const uint32_t p01 = code_pair_dir_pre<lut_tbf(LUT), lut_ks(LUT)>(R01, G01, B01, mk, a0, a1);
-    const uint32_t p23 = code_pair_dir_pre<lut_tbf(LUT), lut_ks(LUT)>(R23, G23, B23, mk, b0, b1);
-    hist_inc(hb, dir_off_lo(p01, lut[a0]));
-    hist_inc(hb, dir_off_hi(p01, lut[a1]));
-    hist_inc(hb, dir_off_lo(p23, lut[b0]));
-    hist_inc(hb, dir_off_hi(p23, lut[b1]));
-  } else if constexpr (LUT) {
-    uint32_t a0, a1, b0, b1;
-    const uint32_t p01 = code_pair_lut_pre<lut_swz(LUT)>(R01, G01, B01, mk, a0, a1);
-    const uint32_t p23 = code_pair_lut_pre<lut_swz(LUT)>(R23, G23, B23, mk, b0, b1);
-    const uint32_t c01 = code_pair_lut_post(p01, lut[a0], lut[a1], mk);
-    const uint32_t c23 = code_pair_lut_post(p23, lut[b0], lut[b1], mk);
-    hist_inc(hb, lut_off_lo(c01, mk));
-    hist_inc(hb, lut_off_hi(c01, mk));
-    hist_inc(hb, lut_off_lo(c23, mk));
-    hist_inc(hb, lut_off_hi(c23, mk));
-  } else {
-    const uint32_t c01 = code_pair(R01, G01, B01, mk);
-    const uint32_t c23 = code_pair(R23, G23, B23, mk);
-    hist_inc(hb, code_off_lo(c01, mk));
-    hist_inc(hb, code_off_hi(c01, mk));
-    hist_inc(hb, code_off_lo(c23, mk));
-    hist_inc(hb, code_off_hi(c23, mk));
-  }
+template <bool IMM>
+__device__ __forceinline__ void hist_inc(uint32_t sb, uint32_t x) {
+  if constexpr (IMM)
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(x), "n"(kDynSmemBase + kHistOff) : "memory");
+  else
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sb + kHistOff + x) : "memory");
 }
 
 // NQ quads of one lane, phase by phase across all of them (loads, unpack,
-// codes, table lookups, atomics): NQ*2 independent pixel-pair chains in flight.
-template <int NQ, int SWZ>
-__device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qstride,
-                                              uint32_t* hist, uint32_t lut_s, MadK mk) {
+// codes, table lookups, atomics): 2 NQ independent pixel-pair chains in flight.
+// Quad j of the lane is the 12 bytes at buf + (q0 + j * qstride) * 12.
+template <int NQ, bool IMM>
+__device__ __forceinline__ void bin_quads(const uint8_t* buf, int q0, int qstride, uint32_t sb,
+                                          MadK mk) {
   uint32_t w[NQ][3];
 #pragma unroll
   for (int j = 0; j < NQ; ++j) {
@@ -291,192 +151,46 @@ __device__ __forceinline__ void bin_quads_lut(const uint8_t* buf, int q0, int qs
 #pragma unroll
   for (int j = 0; j < NQ; ++j) {
     uint32_t R01, G01, B01, R23, G23, B23;
-    unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
-    pre[2 * j] = code_pair_lut_pre<SWZ>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-    pre[2 * j + 1] = code_pair_lut_pre<SWZ>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23);
+    pre[2 * j] = code_pair_dir_pre(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_dir_pre(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
   }
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
-    qa[j] = lds_u8(lut_s + ia[j]);
-    qb[j] = lds_u8(lut_s + ib[j]);
+    qa[j] = lut_ld<IMM>(sb, ia[j]);
+    qb[j] = lut_ld<IMM>(sb, ib[j]);
   }
-  char* hb = reinterpret_cast<char*>(hist);
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
-    const uint32_t c = code_pair_lut_post(pre[j], qa[j], qb[j], mk);
-    hist_inc(hb, lut_off_lo(c, mk));
-    hist_inc(hb, lut_off_hi(c, mk));
+    hist_inc<IMM>(sb, dir_off_lo(pre[j], qa[j]));
+    hist_inc<IMM>(sb, dir_off_hi(pre[j], qb[j]));
   }
 }
 
-// Direct-offset codes (lut 5/6): same phase order as bin_quads_lut; each table
-// entry goes into its atomic's address with one PRMT.
-// OCT = 1: a lane's quads come in adjacent pairs (24 bytes, three LDS.64):
-// quads 2j and 2j+1 of a lane are pixels [8 (q0 + j qstride), +8).
-template <int NQ, int TBF, uint32_t HIST_S, uint32_t LUT_S, int OCT = 0, int KS = 4, int XU = 0>
-__device__ __forceinline__ void bin_quads_dir(const uint8_t* buf, int q0, int qstride, MadK mk) {
-  uint32_t w[NQ][3];
-  if constexpr (OCT == 2) {
-    // a lane's quads come in groups of four (48 bytes, three LDS.128): quads
-    // 4j..4j+3 are pixels [16 (q0 + j qstride), +16); a quarter-warp's 8 lanes
-    // at a 48-byte stride cover 32 distinct banks (conflict-free)
+// 16 pixels (one 48-byte group) with the exact generic bin (any bin layout)
+__device__ __forceinline__ void bin_group_generic(const uint8_t* src, uint32_t* hist, uint32_t nh,
+                                                  uint32_t ns, uint32_t nv) {
+  const uint4* p = reinterpret_cast<const uint4*>(src);
+  const uint4 a = p[0], b = p[1], c = p[2];
+  const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int j = 0; j < NQ / 4; ++j) {
-      const uint4* p = reinterpret_cast<const uint4*>(buf + (q0 + j * qstride) * 48);
-      const uint4 a = p[0], b = p[1], c = p[2];
-      const uint32_t v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-#pragma unroll
-      for (int k = 0; k < 12; ++k) w[4 * j + k / 3][k % 3] = v[k];
-    }
-  } else if constexpr (OCT) {
-#pragma unroll
-    for (int j = 0; j < NQ / 2; ++j) {
-      const uint2* p = reinterpret_cast<const uint2*>(buf + (q0 + j * qstride) * 24);
-      const uint2 a = p[0], b = p[1], c = p[2];
-      w[2 * j][0] = a.x;
-      w[2 * j][1] = a.y;
-      w[2 * j][2] = b.x;
-      w[2 * j + 1][0] = b.y;
-      w[2 * j + 1][1] = c.x;
-      w[2 * j + 1][2] = c.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < NQ; ++j) {
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(buf + (q0 + j * qstride) * 12);
-      w[j][0] = p[0];
-      w[j][1] = p[1];
-      w[j][2] = p[2];
-    }
-  }
-  uint32_t pre[2 * NQ], ia[2 * NQ], ib[2 * NQ];
-#pragma unroll
-  for (int j = 0; j < NQ; ++j) {
-    uint32_t R01, G01, B01, R23, G23, B23;
-    if constexpr (XU) {  // no shifts in the unpack; the offset goes back through kz / km
-      uint32_t off;
-      unpack4x(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, off);
-      const uint32_t kz = cd_mad(off, mk.one, 0x04000400u), km = cd_mad(off, mk.neg3, 0u);
-      pre[2 * j] = code_pair_dir_pre<TBF, KS, 1>(R01, G01, B01, mk, ia[2 * j], ib[2 * j], kz, km);
-      pre[2 * j + 1] =
-          code_pair_dir_pre<TBF, KS, 1>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1], kz, km);
-    } else {
-      unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23, mk);
-      pre[2 * j] = code_pair_dir_pre<TBF, KS>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-      pre[2 * j + 1] = code_pair_dir_pre<TBF, KS>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
-    }
-  }
-  uint32_t qa[2 * NQ], qb[2 * NQ];
-#pragma unroll
-  for (int j = 0; j < 2 * NQ; ++j) {
-#ifdef CLIPDETECT_EXP_NO_TABLE
-    // experiment build only (tools/): a table-free stand-in entry (wrong bins)
-    qa[j] = ia[j] & 0x7Cu;
-    qb[j] = ib[j] & 0x7Cu;
-#else
-    qa[j] = lds_u8(LUT_S + ia[j]);
-    qb[j] = lds_u8(LUT_S + ib[j]);
-#endif
-  }
-#pragma unroll
-  for (int j = 0; j < 2 * NQ; ++j) {
-    hist_inc_s<HIST_S>(dir_off_lo(pre[j], qa[j]));
-    hist_inc_s<HIST_S>(dir_off_hi(pre[j], qb[j]));
+  for (int i = 0; i < 16; ++i) {
+    const int o = 3 * i;
+    const uint32_t r = __byte_perm(w[o >> 2], 0u, 0x4440u | (o & 3));
+    const uint32_t g = __byte_perm(w[(o + 1) >> 2], 0u, 0x4440u | ((o + 1) & 3));
+    const uint32_t bb = __byte_perm(w[(o + 2) >> 2], 0u, 0x4440u | ((o + 2) & 3));
+    atomicAdd(&hist[bin_generic(r, g, bb, nh, ns, nv)], 1u);
   }
 }
 
-template <int MODE, int STAGES, int MINB, int CW, int LUT, int QUAD, int NOPROD, int SG>
-__global__ void __launch_bounds__(CW * 32 + (NOPROD ? 0 : 32), MINB)
-k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
-               uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
-  constexpr int kConsumers = CW * 32;
-  constexpr int kThreads = kConsumers + (NOPROD ? 0 : 32);
-  constexpr int kGPT = SG / kConsumers;  // 0 when a stage has fewer groups than lanes
-  static_assert(kGPT == 0 || kGPT * kConsumers == SG || QUAD, "stage must split evenly");
-  constexpr bool kUseLut = (MODE == kModeFast) && LUT;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  K1Smem<STAGES, LUT, SG>& sm = *reinterpret_cast<K1Smem<STAGES, LUT, SG>*>(smem_raw);
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+// The consumer loop (IMM: see lut_ld).
+template <int MODE, bool IMM>
+__device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const HistSeg* segs,
+                                           int32_t nseg, int64_t s_begin, int32_t n, uint32_t nh,
+                                           uint32_t ns, uint32_t nv, uint32_t* sink) {
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t nbins = nh * ns * nv;
-
-  const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
-  const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
-  if ((uint32_t)__cvta_generic_to_shared(smem_raw) != kDynSmemBase) __trap();  // see lut_s
-
-  constexpr int kEntries = K1Smem<STAGES, LUT, SG>::kEntries;
-  const uint32_t nentries = MODE == kModeFast ? (uint32_t)kEntries : nbins;
-  for (int i = tid; i < kEntries; i += kThreads) sm.hist[i] = 0u;
-  for (int i = tid; i < 256; i += kThreads) sm.binacc[i] = 0u;
-  if (MODE == kModeFast)
-    for (int i = tid; i < kEntries; i += kThreads)
-      sm.c2b[i] = (uint8_t)(lut_dir(LUT) ? code_to_bin_dir(i)
-                                         : (kUseLut ? code_to_bin_lut(i) : code_to_bin(i)));
-  if (kUseLut)
-    for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8,
-                     na = lut_dir(LUT) ? lut_unswizzle_k((uint32_t)i & 255u, d, lut_ks(LUT))
-                                       : lut_unswizzle((uint32_t)i & 255u, d, lut_swz(LUT));
-      sm.lut[i] = (uint8_t)(na > d ? 0u
-                                   : (lut_dir(LUT) ? lut_entry_dir(na, d, lut_hash(LUT)) : lut_entry(na, d)));
-    }
-  if (tid == 0) {
-    sm.mk = mk_param;
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], CW);
-      sm.cnt[i] = 0u;
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (s_begin >= s_end) return;
-
-  // noprod: the first STAGES copies come from thread 0; `ahead` tracks the stage
-  // a slot is refilled with (i + STAGES) in every warp
-  StageIter<SG> ahead;
-  uint64_t pol = 0;
-  if constexpr (NOPROD) {
-    pol = policy_evict_first();
-    const int32_t n = (int32_t)(s_end - s_begin);
-    ahead.seek(segs, nseg, s_begin);
-    for (int32_t i = 0; i < STAGES && i < n; ++i) {
-      if (tid == 0) {
-        const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
-        const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * SG) * 48;
-        mbar_arrive_expect_tx(&sm.full[i], bytes);
-        bulk_g2s(sm.buf[i], src, bytes, &sm.full[i], pol);
-      }
-      ahead.next(i + 1 < n);
-    }
-  }
-
-  if (!NOPROD && warp == CW) {
-    // ---------------------------------------------------------- producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      StageIter<SG> it;
-      it.seek(segs, nseg, s_begin);
-      const int32_t n = (int32_t)(s_end - s_begin);
-      uint32_t slot = 0, par = 0;
-      for (int32_t i = 0; i < n; ++i) {
-        if (i >= STAGES) mbar_wait(&sm.empty[slot], par ^ 1u);
-        const uint32_t bytes = (uint32_t)it.ng() * 48u;
-        const uint8_t* src = it.frames + ((int64_t)it.frame * it.groups + (int64_t)it.st * SG) * 48;
-        mbar_arrive_expect_tx(&sm.full[slot], bytes);
-        bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
-        it.next(i + 1 < n);
-        if (++slot == STAGES) {
-          slot = 0;
-          par ^= 1u;
-        }
-      }
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------ consumers
   // multiplier constants through shared memory: opaque registers for ptxas
   MadK mk;
   {
@@ -485,107 +199,44 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
 #pragma unroll
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
-  uint32_t* wh = sm.hist;
-  using Smem = K1Smem<STAGES, LUT, SG>;
-  // The hue table's 32-bit shared-window address as a compile-time constant:
-  // dynamic shared memory starts after the 1 KiB the system reserves, at
-  // kDynSmemBase, for a launch without clusters (checked at kernel entry), so
-  // each table load is LDS [index + imm] with no per-load base add.
-  constexpr uint32_t lut_s = kDynSmemBase + (uint32_t)offsetof(Smem, lut);
   uint32_t xacc = 0;
-  StageIter<SG> it;
+  StageIter it;
   it.seek(segs, nseg, s_begin);
-  const int32_t n = (int32_t)(s_end - s_begin);
   uint32_t slot = 0, par = 0;
   for (int32_t i = 0; i < n; ++i) {
     const int ng = it.ng();
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
-    if constexpr (QUAD == 1 && MODE == kModeFast) {
-      const int nq = ng * 4;
-#pragma unroll 2
-      for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
-    } else if constexpr ((QUAD == 4 || QUAD == 5) && MODE == kModeFast && lut_dir(LUT)) {
-      // lane-contiguous octets (QUAD 4: 24 bytes, three LDS.64) or 16-pixel
-      // groups (QUAD 5: 48 bytes, three LDS.128), direct-offset codes
-      constexpr int kQPL = 4 * SG / kConsumers;
-      const int nq = ng * 4;
-      if (nq == kQPL * kConsumers) {
-        bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s,
-                      QUAD == 5 ? 2 : 1, lut_ks(LUT)>(buf, tid, kConsumers, mk);
-      } else {
-        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
+    if constexpr (MODE == kModeFast) {
+      if (ng == kStageGroups) {
+        bin_quads<kQPL, IMM>(buf, tid, kConsumers, sbase, mk);
+      } else {  // ragged last stage of a frame: quad by quad
+        for (int q = tid; q < ng * 4; q += kConsumers) bin_quads<1, IMM>(buf, q, 0, sbase, mk);
       }
-    } else if constexpr (QUAD == 3 && MODE == kModeFast && LUT) {
-      constexpr int kQPL = 4 * SG / kConsumers;
-      const int nq = ng * 4;
-      if (nq == kQPL * kConsumers) {
-        if constexpr (lut_dir(LUT))
-          bin_quads_dir<kQPL, lut_tbf(LUT), kDynSmemBase + (uint32_t)offsetof(Smem, hist), lut_s, 0,
-                        lut_ks(LUT), lut_xu(LUT)>(
-              buf, tid, kConsumers, mk);
-        else
-          bin_quads_lut<kQPL, lut_swz(LUT)>(buf, tid, kConsumers, wh, lut_s, mk);
-      } else {
-        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
-      }
-    } else if constexpr (QUAD == 2 && MODE == kModeFast) {
-      // all of a lane's quads of a full stage issued together (more independent work per warp)
-      constexpr int kQPL = 4 * SG / kConsumers;
-      const int nq = ng * 4;
-      if (nq == kQPL * kConsumers) {
-#pragma unroll
-        for (int j = 0; j < kQPL; ++j) bin_quad<LUT>(buf + (tid + j * kConsumers) * 12, wh, sm.lut, mk);
-      } else {
-        for (int q = tid; q < nq; q += kConsumers) bin_quad<LUT>(buf + q * 12, wh, sm.lut, mk);
-      }
-    } else if constexpr (kGPT == 0) {
-      if (tid < ng) bin_group<MODE, LUT>(buf + tid * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
-    } else {
-#pragma unroll
-      for (int j = 0; j < kGPT; ++j) {
-        const int gi = tid + j * kConsumers;
-        if (gi < ng) bin_group<MODE, LUT>(buf + gi * 48, wh, sm.lut, nh, ns, nv, mk, xacc);
+    } else if constexpr (MODE == kModeGeneric) {
+      for (int gi = tid; gi < ng; gi += kConsumers) bin_group_generic(buf + gi * 48, sm.hist, nh, ns, nv);
+    } else {  // kModeRead: touch every byte, no binning
+      for (int gi = tid; gi < ng; gi += kConsumers) {
+        const uint4* p = reinterpret_cast<const uint4*>(buf + gi * 48);
+        const uint4 a = p[0], b = p[1], c = p[2];
+        xacc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w;
       }
     }
     __syncwarp();
-    if constexpr (NOPROD) {
-      if (lane == 0 && atomicAdd(&sm.cnt[slot], 1u) == (uint32_t)(CW - 1)) {
-        // last warp out of this slot: refill it with stage i + STAGES
-        sm.cnt[slot] = 0u;
-        if (i + STAGES < n) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const uint32_t bytes = (uint32_t)ahead.ng() * 48u;
-          const uint8_t* src = ahead.frames + ((int64_t)ahead.frame * ahead.groups + (int64_t)ahead.st * SG) * 48;
-          mbar_arrive_expect_tx(&sm.full[slot], bytes);
-          bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
-        }
-      }
-      if (i + STAGES < n) ahead.next(i + STAGES + 1 < n);
-    } else {
-      if (lane == 0) mbar_arrive(&sm.empty[slot]);
-    }
-    if (++slot == STAGES) {
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    if (++slot == kStages) {
       slot = 0;
       par ^= 1u;
     }
-
     const int32_t seg_now = it.seg, frame_now = it.frame;
     const bool last = (i + 1 == n);
     const bool changed = it.next(!last);
-#ifdef CLIPDETECT_EXP_NO_FLUSH
-    // experiment build only (tools/): flush once at the end (wrong per-frame bins)
-    const bool flush_now = last;
-#else
-    const bool flush_now = last || changed;
-#endif
-    if (MODE != kModeRead && flush_now) {
+    if (MODE != kModeRead && (last || changed)) {
       // flush the frame's partial code histogram straight to the frame's global
-      // bins: one RED per non-zero code, two barriers (the older two-level flush
-      // through a shared bin histogram took three; +0.2-0.8 % K1, identical bins,
-      // profiles/r01/flush/)
+      // bins: one RED per non-zero code, two named barriers among the consumers
       named_bar_sync(1, kConsumers);
       uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
+      const uint32_t nentries = MODE == kModeFast ? (uint32_t)kDirCodes : nbins;
       for (uint32_t c = tid; c < nentries; c += kConsumers) {
         const uint32_t cnt = sm.hist[c];
         if (cnt) {
@@ -599,142 +250,115 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   if (MODE == kModeRead && xacc == 0x9E3779B9u) sink[0] = xacc;  // keep the loads alive
 }
 
-template <int MODE, int C>
-struct Cfg {
-  static constexpr int S = kCfgs[C].stages, M = kCfgs[C].ctas_per_sm, W = kCfgs[C].warps,
-                       L = kCfgs[C].lut, Q = kCfgs[C].quad, NP = kCfgs[C].noprod, G = kCfgs[C].sg;
-  static constexpr int kThreads = W * 32 + (NP ? 0 : 32);
-  static constexpr auto kernel() { return k1_hist_kernel<MODE, S, M, W, L, Q, NP, G>; }
-  static constexpr size_t smem() { return sizeof(K1Smem<S, L, G>); }
-};
-
-template <int MODE, int C>
-cudaError_t launch_cfg(const HistSeg* d_segs, int32_t nseg, int64_t total_stages, uint32_t nh,
-                       uint32_t ns, uint32_t nv, uint32_t* sink, int grid, cudaStream_t stream) {
-  using K = Cfg<MODE, C>;
-  K::kernel()<<<grid, K::kThreads, K::smem(), stream>>>(d_segs, nseg, total_stages, nh, ns,
-                                                             nv, kMadK, sink);
-  return cudaGetLastError();
-}
-
-// cfg (runtime) -> launch_cfg<MODE, cfg> over every configuration; unknown -> 0
-template <int MODE, int... C>
-cudaError_t launch_any(std::integer_sequence<int, C...>, int cfg, const HistSeg* d_segs,
-                       int32_t nseg, int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
-                       uint32_t* sink, int grid, cudaStream_t stream) {
-  cudaError_t e = cudaErrorInvalidValue;
-  const bool hit = ((cfg == C ? (e = launch_cfg<MODE, C>(d_segs, nseg, total_stages, nh, ns, nv,
-                                                          sink, grid, stream),
-                                 true)
-                              : false) || ...);
-  return hit ? e : launch_cfg<MODE, 0>(d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-}
-
 template <int MODE>
-cudaError_t launch_mode(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
-                        uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid,
-                        cudaStream_t stream) {
-  return launch_any<MODE>(std::make_integer_sequence<int, kNumCfgs>{}, cfg, d_segs, nseg,
-                          total_stages, nh, ns, nv, sink, grid, stream);
-}
+__global__ void __launch_bounds__(kThreads, 1)
+k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
+               uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t s_begin = total_stages * blockIdx.x / gridDim.x;
+  const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
 
-template <int MODE, int C>
-cudaError_t configure_cfg() {
-  using K = Cfg<MODE, C>;
-  return cudaFuncSetAttribute(K::kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)K::smem());
-}
+  if (MODE != kModeRead) {
+    for (int i = tid; i < kDirCodes; i += kThreads) sm.hist[i] = 0u;
+  }
+  if (MODE == kModeFast) {
+    for (int i = tid; i < kDirCodes; i += kThreads) sm.c2b[i] = (uint8_t)code_to_bin_dir(i);
+    for (int i = tid; i < kLutBytes; i += kThreads) {
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d);
+      sm.lut[i] = (uint8_t)(na > d ? 0u : lut_entry_dir(na, d, kHashRgb));
+    }
+  }
+  if (tid == 0) {
+    sm.mk = mk_param;
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (s_begin >= s_end) return;
+  const int32_t n = (int32_t)(s_end - s_begin);
 
-// the shared-memory opt-in of every configuration's kernel; first error wins
-template <int MODE, int... C>
-cudaError_t configure_all(std::integer_sequence<int, C...>) {
-  cudaError_t e = cudaSuccess;
-  ((e == cudaSuccess ? (e = configure_cfg<MODE, C>(), 0) : 0), ...);
-  return e;
-}
-
-template <int MODE>
-cudaError_t configure_mode() {
-  return configure_all<MODE>(std::make_integer_sequence<int, kNumCfgs>{});
+  if (warp == kWarps) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      StageIter it;
+      it.seek(segs, nseg, s_begin);
+      uint32_t slot = 0, par = 0;
+      for (int32_t i = 0; i < n; ++i) {
+        if (i >= kStages) mbar_wait(&sm.empty[slot], par ^ 1u);
+        const uint32_t bytes = (uint32_t)it.ng() * 48u;
+        mbar_arrive_expect_tx(&sm.full[slot], bytes);
+        bulk_g2s(sm.buf[slot], it.src(), bytes, &sm.full[slot], pol);
+        it.next(i + 1 < n);
+        if (++slot == kStages) {
+          slot = 0;
+          par ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  const uint32_t sbase = smem_u32(smem_raw);
+  if (sbase == kDynSmemBase)
+    k1_consume<MODE, true>(sm, sbase, segs, nseg, s_begin, n, nh, ns, nv, sink);
+  else
+    k1_consume<MODE, false>(sm, sbase, segs, nseg, s_begin, n, nh, ns, nv, sink);
 }
 
 }  // namespace
 
-// K1_TU (build only): hist.cu is compiled once per mode (K1_TU = 0 fast +
-// shared entry points and K5, 1 generic, 2 read) so that the instantiations of
-// every launch configuration compile in parallel; undefined = everything here.
-#ifndef K1_TU
-#define K1_TU -1
-#endif
-#define K1_DECL_MODE(NAME)                                                                     \
-  cudaError_t k1_configure_##NAME();                                                           \
-  cudaError_t k1_launch_##NAME(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total,    \
-                               uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid, \
-                               cudaStream_t stream);
-#define K1_DEF_MODE(NAME, MODE)                                                                \
-  cudaError_t k1_configure_##NAME() { return configure_mode<MODE>(); }                         \
-  cudaError_t k1_launch_##NAME(int cfg, const HistSeg* d_segs, int32_t nseg, int64_t total,    \
-                               uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int grid, \
-                               cudaStream_t stream) {                                          \
-    return launch_mode<MODE>(cfg, d_segs, nseg, total, nh, ns, nv, sink, grid, stream);        \
-  }
-K1_DECL_MODE(fast)
-K1_DECL_MODE(generic)
-K1_DECL_MODE(read)
-#if K1_TU < 0 || K1_TU == 0
-K1_DEF_MODE(fast, kModeFast)
-#endif
-#if K1_TU < 0 || K1_TU == 1
-K1_DEF_MODE(generic, kModeGeneric)
-#endif
-#if K1_TU < 0 || K1_TU == 2
-K1_DEF_MODE(read, kModeRead)
-#endif
-
-#if K1_TU < 0 || K1_TU == 0
-int k1_stage_groups(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].sg : kStageGroups; }
-int k1_num_cfgs() { return kNumCfgs; }
+int64_t k1_stages(int64_t groups) { return (groups + kStageGroups - 1) / kStageGroups; }
 
 cudaError_t k1_configure() {
   cudaError_t e;
-  if ((e = k1_configure_fast()) != cudaSuccess) return e;
-  if ((e = k1_configure_generic()) != cudaSuccess) return e;
-  return k1_configure_read();
+  if ((e = cudaFuncSetAttribute(k1_hist_kernel<kModeFast>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(K1Smem))) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k1_hist_kernel<kModeGeneric>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(K1Smem))) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(k1_hist_kernel<kModeRead>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(K1Smem));
 }
 
-int k1_grid(int cfg, int sm_count, int64_t total_stages) {
-  if (cfg < 0 || cfg >= kNumCfgs) cfg = 0;
-  int64_t g = (int64_t)sm_count * kCfgs[cfg].ctas_per_sm;
-  if (total_stages < g) g = total_stages;
-  return (int)(g < 1 ? 1 : g);
-}
-
-cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
-                      int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
-                      uint32_t* sink, int grid, cudaStream_t stream) {
+cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
+                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
+                      cudaStream_t stream) {
   if (total_stages <= 0) return cudaSuccess;
+  const int grid = (int)(total_stages < sm_count ? total_stages : sm_count);
+  const size_t smem = sizeof(K1Smem);
   if (mode == kModeFast)
-    return k1_launch_fast(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-  if (mode == kModeGeneric)
-    return k1_launch_generic(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
-  return k1_launch_read(cfg, d_segs, nseg, total_stages, nh, ns, nv, sink, grid, stream);
+    k1_hist_kernel<kModeFast><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh, ns,
+                                                                nv, kMadK, sink);
+  else if (mode == kModeGeneric)
+    k1_hist_kernel<kModeGeneric><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh,
+                                                                   ns, nv, kMadK, sink);
+  else
+    k1_hist_kernel<kModeRead><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh, ns,
+                                                                nv, kMadK, sink);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- K5 (test)
 // The hot-path bin evaluation over all 2^24 colours: colour c in lane 0 and
-// colour c ^ 0xA5A5A5 in lane 1 of the two-pixel code, through the same code
-// -> bin tables (and, for the LUT variant, the same shared-memory hue table)
-// as K1.  out[0][c] = lane-0 result, out[1][c] = lane-1 result.
+// colour c ^ 0xA5A5A5 in lane 1 of the two-pixel code, through the same hue
+// table and code -> bin map as K1 (fast = 0: bin_generic for other layouts).
+// out[0][c] = lane-0 result, out[1][c] = lane-1 result.
 namespace {
-template <int LUT>
 __global__ void __launch_bounds__(256)
-k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                 MadK mk, int hash, int ks) {
+k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t nv, int fast, MadK mk) {
   extern __shared__ __align__(16) uint8_t lut[];
-  if (LUT) {
+  if (fast) {
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle_k((uint32_t)i & 255u, d, (uint32_t)ks);
-      lut[i] = (uint8_t)(na > d ? 0u : (LUT == 2 ? lut_entry_dir(na, d, hash) : lut_entry(na, d)));
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d);
+      lut[i] = (uint8_t)(na > d ? 0u : lut_entry_dir(na, d, kHashRgb));
     }
     __syncthreads();
   }
@@ -748,54 +372,25 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
     const uint32_t c2 = c ^ 0xA5A5A5u;
     const uint32_t R = r | ((c2 >> 16) << 16), G = g | (((c2 >> 8) & 255u) << 16),
                    B = b | ((c2 & 255u) << 16);
-    uint32_t b0, b1;
-    if (LUT == 2) {  // direct-offset codes (K1 lut 5/6; TBF only moves B between pipes)
-      uint32_t i0, i1;
-      const uint32_t pre = ks == 5 ? code_pair_dir_pre<0, 5>(R, G, B, mk, i0, i1)
-                                   : code_pair_dir_pre<0, 4>(R, G, B, mk, i0, i1);
-      uint32_t j0, j1;
-      const uint32_t pre6 = ks == 5 ? code_pair_dir_pre<1, 5>(R, G, B, mk, j0, j1)
-                                    : code_pair_dir_pre<1, 4>(R, G, B, mk, j0, j1);
-      const uint32_t pre13 = ks == 5 ? code_pair_dir_pre<2, 5>(R, G, B, mk, j0, j1)
-                                     : code_pair_dir_pre<2, 4>(R, G, B, mk, j0, j1);
-      if (pre13 != pre) b0 = b1 = 253u;
-      b0 = code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);
-      b1 = code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);
-      if (pre6 != pre || pre13 != pre || j0 != i0 || j1 != i1) b0 = b1 = 254u;
-    } else if (LUT) {
-      uint32_t i0, i1;
-      const uint32_t pre = code_pair_lut_pre(R, G, B, mk, i0, i1);
-      const uint32_t code = code_pair_lut_post(pre, lut[i0], lut[i1], mk);
-      b0 = code_to_bin_lut(lut_off_lo(code, mk) >> 2);
-      b1 = code_to_bin_lut(lut_off_hi(code, mk) >> 2);
-    } else {
-      const uint32_t code = code_pair(R, G, B, mk);
-      b0 = code_to_bin(code_off_lo(code, mk) >> 2);
-      b1 = code_to_bin(code_off_hi(code, mk) >> 2);
-    }
-    out[c] = (uint8_t)b0;                // table 0: lane 0
-    out[(1u << 24) + c2] = (uint8_t)b1;  // table 1: lane 1
+    uint32_t i0, i1;
+    const uint32_t pre = code_pair_dir_pre(R, G, B, mk, i0, i1);
+    out[c] = (uint8_t)code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);                // lane 0
+    out[(1u << 24) + c2] = (uint8_t)code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);  // lane 1
   }
 }
 }  // namespace
 
-int k1_cfg_uses_lut(int cfg) { return (cfg >= 0 && cfg < kNumCfgs) ? kCfgs[cfg].lut : 0; }
-
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                             int lut, cudaStream_t stream) {
-  if (fast && lut >= 5) {
-    cudaFuncSetAttribute(k5_binmap_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
-    k5_binmap_kernel<2><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK, lut_hash(lut),
-                                                             lut_ks(lut));
-  } else if (fast && lut) {
-    cudaFuncSetAttribute(k5_binmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutBytes);
-    k5_binmap_kernel<1><<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK, 0, 4);
+                             cudaStream_t stream) {
+  if (fast) {
+    cudaError_t e = cudaFuncSetAttribute(k5_binmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kLutBytes);
+    if (e != cudaSuccess) return e;
+    k5_binmap_kernel<<<kSMs, 256, kLutBytes, stream>>>(out, nh, ns, nv, fast, kMadK);
   } else {
-    k5_binmap_kernel<0><<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, fast, kMadK, 0, 4);
+    k5_binmap_kernel<<<kSMs * 8, 256, 0, stream>>>(out, nh, ns, nv, fast, kMadK);
   }
   return cudaGetLastError();
 }
-
-#endif  // K1_TU
 
 }  // namespace clipdetect

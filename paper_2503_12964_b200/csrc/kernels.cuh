@@ -11,16 +11,14 @@ namespace clipdetect {
 enum { kModeFast = 0, kModeGeneric = 1, kModeRead = 2 };
 
 // ---- K1 (hist.cu)
-int k1_stage_groups(int cfg);  // 48-byte groups per K1 stage of a launch configuration
-int k1_num_cfgs();
+int64_t k1_stages(int64_t groups);  // K1 stages of a frame of `groups` 48-byte groups
 cudaError_t k1_configure();
-int k1_grid(int cfg, int sm_count, int64_t total_stages);
-cudaError_t k1_launch(int mode, int cfg, const HistSeg* d_segs, int32_t nseg,
-                      int64_t total_stages, uint32_t nh, uint32_t ns, uint32_t nv,
-                      uint32_t* sink, int grid, cudaStream_t stream);
-int k1_cfg_uses_lut(int cfg);
+// persistent grid of min(total_stages, sm_count) CTAs
+cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
+                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
+                      cudaStream_t stream);
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                             int lut, cudaStream_t stream);
+                             cudaStream_t stream);
 
 // ---- K1 for NV12 input (hist_nv12.cu)
 int nv12_stage_rows(int32_t width);
@@ -31,9 +29,9 @@ cudaError_t k1_nv12_configure();
 // kModeGeneric: generic kernel over `total` (frame, 8-block-row) items.
 cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
                            uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                           int dir, cudaStream_t stream);
+                           cudaStream_t stream);
 cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
-                              int dir, cudaStream_t stream);
+                              cudaStream_t stream);
 
 // ---- K4 (sample.cu): clip frame sampling + resize (NEXT f3)
 int k4_rows_per_band(int32_t W, bool nv12);

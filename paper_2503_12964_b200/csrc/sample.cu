@@ -167,12 +167,7 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
 
 int k4_rows_per_band(int32_t W, bool nv12) {
   const int32_t slot = (((nv12 ? W : 3 * W) + 32) + 15) & ~15;
-  int32_t budget = kK4SmemRows;
-  if (const char* e = getenv("CLIPDETECT_K4_BUDGET_KB")) {  // tuning hook (tools/k4_micro.py)
-    const int kb = atoi(e);
-    if (kb >= 4 && kb <= 200) budget = kb * 1024;
-  }
-  int32_t rb = budget / ((nv12 ? 4 : 2) * slot);
+  int32_t rb = kK4SmemRows / ((nv12 ? 4 : 2) * slot);
   if (rb > (nv12 ? 16 : 32)) rb = nv12 ? 16 : 32;
   return rb < 1 ? 1 : rb;
 }

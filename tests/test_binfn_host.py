@@ -1,7 +1,9 @@
-"""The device bin code (csrc/binfn.cuh: code_pair + code_to_bin, unpack4 and
-bin_generic), compiled for the HOST with its CUDA intrinsics emulated, equals
-the oracle's O1 bin on all 2^24 colours in both u16x2 lanes.  The same
-functions are checked on the GPU by K5 (tests/test_gpu_parity.py)."""
+"""The device bin code (csrc/binfn.cuh: code_pair_dir_pre + the hue table +
+code_to_bin_dir, unpack4, the NV12 conversion and bin_generic), compiled for
+the HOST with its CUDA intrinsics emulated, equals the oracle's O1 bin (and
+O0 then O1 for NV12) on all 2^24 inputs in both u16x2 lanes.  The same
+functions are checked on the GPU by K5 (tests/test_gpu_parity.py,
+tests/test_gpu_nv12.py)."""
 import os
 import subprocess
 
@@ -29,20 +31,14 @@ def test_device_bin_code_on_host_all_colours(exe, tmp_path, bins):
     subprocess.check_call([exe, path, *map(str, bins)])
     raw = np.fromfile(path, dtype=np.uint8)
     n = 1 << 24
-    t0, t1, tg, l0, l1, n0, n1, e0, e1, m0, m1 = (raw[i * n:(i + 1) * n] for i in range(11))
+    e0, e1, tg, m0, m1 = (raw[i * n:(i + 1) * n] for i in range(5))
     p = oracle.Params(nh=bins[0], ns=bins[1], nv=bins[2])
     want = oracle.bin_table(p)
     assert np.array_equal(tg, want)
     if bins == (18, 3, 3):
-        assert np.array_equal(t0, want), np.nonzero(t0 != want)[0][:10]
-        assert np.array_equal(t1, want), np.nonzero(t1 != want)[0][:10]
-        assert np.array_equal(l0, want), np.nonzero(l0 != want)[0][:10]
-        assert np.array_equal(l1, want), np.nonzero(l1 != want)[0][:10]
-        assert np.array_equal(e0, want), np.nonzero(e0 != want)[0][:10]  # direct-offset codes
-        assert np.array_equal(e1, want), np.nonzero(e1 != want)[0][:10]
+        assert np.array_equal(e0, want), np.nonzero(e0 != want)[0][:10]  # K1 codes, lane 0
+        assert np.array_equal(e1, want), np.nonzero(e1 != want)[0][:10]  # lane 1
         yuv = want[yuv_rgb_table()]  # bin of every (Y, U, V): oracle O0 then O1
-        assert np.array_equal(n0, yuv), np.nonzero(n0 != yuv)[0][:10]
-        assert np.array_equal(n1, yuv), np.nonzero(n1 != yuv)[0][:10]
-        assert np.array_equal(m0, yuv), np.nonzero(m0 != yuv)[0][:10]  # direct-offset codes
+        assert np.array_equal(m0, yuv), np.nonzero(m0 != yuv)[0][:10]  # K1-NV12 codes
         assert np.array_equal(m1, yuv), np.nonzero(m1 != yuv)[0][:10]
 

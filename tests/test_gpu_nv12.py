@@ -82,15 +82,12 @@ def test_nv12_scores_random(ctx, dev, W, H, n):
     _check(ctx, random_nv12(rng, n, H, W))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
-def test_nv12_every_code_layout(dev, variant, monkeypatch):
-    """Every K1-NV12 code layout (CLIPDETECT_NV12_DIR: LUT codes, direct
-    offsets with each bank hash / table swizzle) gives the oracle's histograms
-    on random and structured surfaces, and the all-(Y,U,V) bin map."""
+def test_nv12_random_and_structured_with_map(dev):
+    """K1-NV12 gives the oracle's histograms on random and structured surfaces
+    in a fresh context, and the all-(Y,U,V) bin map equals the oracle's."""
     from paper_2503_12964_b200 import Ctx
-    monkeypatch.setenv("CLIPDETECT_NV12_DIR", str(variant))
     c = Ctx(device=0)
-    rng = np.random.default_rng(100 + variant)
+    rng = np.random.default_rng(106)
     _check(c, random_nv12(rng, 3, 720, 1280))
     _check(c, random_nv12(rng, 4, 240, 320, structured=True))
     got = c.debug_nv12map().cpu().numpy()
