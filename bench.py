@@ -29,6 +29,36 @@ METRIC = "decoded frames/sec & HBM GB/s (fraction of peak) at 1/2/4/8 B200 vs CP
 HIST_BYTES = 162 * 4
 
 
+KERNEL_SOURCES = {"k1": ["hist.cu", "binfn.cuh", "common.cuh"],
+                  "k1_nv12": ["hist_nv12.cu", "binfn.cuh", "common.cuh"]}
+
+
+def kernel_src_sha(kind: str) -> str:
+    """sha256 (16 hex) of the kernel's source files: ties an ncu traffic file to
+    the code it was captured from (the GPU box has no .git)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES[kind]:
+        with open(os.path.join(ROOT, "paper_2503_12964_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def traffic_file(kind: str):
+    """(dram bytes per algorithmic byte, thread-instr/px, note) from
+    profiles/<kind>_traffic.json if it was captured from the current sources."""
+    path = os.path.join(ROOT, "profiles", f"{kind}_traffic.json")
+    if not os.path.exists(path):
+        return None, None, "no capture"
+    try:
+        tr = json.load(open(path))
+    except Exception:
+        return None, None, "unreadable capture"
+    if tr.get("src_sha") != kernel_src_sha(kind):
+        return None, None, f"stale capture ({path}: src_sha {tr.get('src_sha')} != {kernel_src_sha(kind)})"
+    return tr["dram_bytes_per_alg_byte"], tr.get("thread_instr_per_px"), tr.get("source")
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -368,6 +398,18 @@ def run_ours(args):
                "note": f"pinned host {'NV12' if nv12 else 'RGB24'} frames + embeddings copied H2D inside the timed region "
                        "(PCIe-bound); detected/final cut lists copied D2H"}
 
+    # ---- worst-case content: K1 on uniform-noise 1080p frames (every rank; rank 0 reports)
+    if "frames" in locals():
+        del frames
+    torch.cuda.empty_cache()
+    noise = None if args.no_noise else k1_noise(dev, stream)
+
+    # ---- north star's C3 strong scaling (64 x 1080p videos, 716.6 GB) at this N:
+    # frames streamed through the device generator at EVERY N (one clock at every N)
+    c3 = None
+    if not args.no_c3:
+        c3 = time_batch("C3", world, rank, dev, local, args.c3_steps, 1, force_stream=True)
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -379,16 +421,8 @@ def run_ours(args):
     k1_ms = st["k1_ms"] / max(1, st["k1_launches"])
     k1_alg = frame_bytes + v.n * HIST_BYTES
     achieved = k1_alg / (k1_ms * 1e-3) / 1e9
-    traffic = None
-    instr_px = None
-    tpath = os.path.join(ROOT, "profiles", "k1_nv12_traffic.json" if nv12 else "k1_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tr = json.load(open(tpath))
-            traffic = int(tr["dram_bytes_per_alg_byte"] * k1_alg)
-            instr_px = tr.get("thread_instr_per_px")
-        except Exception:
-            traffic = None
+    ratio, instr_px, traffic_src = traffic_file("k1_nv12" if nv12 else "k1")
+    traffic = None if ratio is None else int(ratio * k1_alg)
     fps = world * v.n / (ms_step * 1e-3)
     gbs = world * frame_bytes / (ms_step * 1e-3) / 1e9
     # the binding resource of K1 is instruction issue: issue roofline
@@ -435,7 +469,8 @@ def run_ours(args):
                      "kernel": "k1_nv12_kernel" if nv12 else "k1_hist_kernel",
                      "alg_bytes_per_launch": k1_alg, "launch_ms": round(k1_ms, 4), "peak_src": peak_src,
                      "frac_of_read_ceiling": None if read_gbs is None else round(achieved / read_gbs, 4),
-                     "frac_of_8tbs": round(achieved / 8000.0, 4), "instr_per_px_ncu": instr_px},
+                     "frac_of_8tbs": round(achieved / 8000.0, 4), "instr_per_px_ncu": instr_px,
+                     "traffic_src": traffic_src},
         "roofline_issue": issue,
         "kernel_ms_per_step": {"k1": round(st["k1_ms"] / args.steps, 4),
                                "k2": round(st["k2_ms"] / args.steps, 4),
@@ -448,6 +483,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
+    line["k1_noise"] = noise
+    line["c3_strong"] = c3
     if f3 is not None:
         f3["roofline"]["peak"] = peak
         f3["roofline"]["frac"] = round(f3["roofline"]["achieved"] / peak, 4)
@@ -459,14 +496,19 @@ def run_ours(args):
 
 
 # ---------------------------------------------------------------- batch configs (C3/C4/C5)
-def run_config(args):
-    """--config C3|C4|C5: the config's videos LPT-sharded by whole video over the
-    ranks (strong scaling: the batch is fixed).  A rank whose share fits in HBM
-    keeps it resident and is timed with CUDA events around whole steps; a rank
-    whose share does not fit streams frames through clip_run_videos' fill
-    callback (device generator) and is timed by the library's per-kernel CUDA
-    events (K1+K2+K3; generation excluded) — the JSON says which."""
-    import numpy as np
+def time_batch(name, world, rank, dev, local, steps, warmup, resident_gb=150.0,
+               force_stream=False, max_videos=0):
+    """One config's videos LPT-sharded by whole video over the ranks (strong
+    scaling: the batch is fixed) and timed the same way at every N.
+
+    Frames are resident in HBM when the LARGEST rank share fits in
+    `resident_gb` (every rank knows every share: no collective) and
+    `force_stream` is off; otherwise EVERY rank streams its frames chunk by
+    chunk through clip_run_videos' fill callback (the device generator writes
+    each chunk into the library's staging buffer on the ctx stream: synthetic
+    "decode" inside the step).  Two clocks, both max over ranks: `wall` = CUDA
+    events around whole steps (clip_run_videos + the one all-gather of the cut
+    lists), `kernel` = the library's CUDA events around K1 + K2 + K3."""
     import torch
     import torch.distributed as dist
 
@@ -475,21 +517,13 @@ def run_config(args):
     from paper_2503_12964_b200 import Ctx
     from paper_2503_12964_b200 import dist as cdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    synth.build(device=True)
-    vids = manifest.config_videos(args.config)
-    if args.max_videos:
-        vids = vids[:args.max_videos]
+    vids = manifest.config_videos(name)
+    if max_videos:
+        vids = vids[:max_videos]
     assign = cdist.lpt_assign([v.n * v.W * v.H for v in vids], world)
+    share = [sum(vids[i].n * vids[i].frame_bytes for i in a) for a in assign]
+    resident = (not force_stream) and max(share) <= resident_gb * 1e9
     mine = [vids[i] for i in assign[rank]]
-    my_bytes = sum(v.n * v.frame_bytes for v in mine)
-    resident = my_bytes <= args.resident_gb * 1e9
     tables = [torch_dev.frame_table(v, dev) for v in mine]
     items = []
     for v, t in zip(mine, tables):
@@ -510,80 +544,158 @@ def run_config(args):
     stream = torch.cuda.Stream(device=dev)
     ctx = Ctx(device=local, stream=stream, timing=True)
     cap = cdist.capacity_ints([v.n for v in vids], 8)
-    out = [None, None]
+    out = [None]
+    gather_s = [0.0]
 
     def step():
         with torch.cuda.stream(stream):
             res = ctx.run_videos(items, fill=None if resident else fill) if items else []
-            out[0] = res
             if world > 1:
-                out[1] = cdist.gather_results(res, cap, device=dev)
+                t0 = time.perf_counter()
+                out[0] = cdist.gather_results(res, cap, device=dev)
+                gather_s[0] += time.perf_counter() - t0
             else:
-                out[1] = [{"id": r.id, "detected": r.detected, "final": r.final} for r in res]
+                out[0] = [{"id": r.id, "detected": r.detected, "final": r.final} for r in res]
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     ctx.stats(reset=True)
+    gather_s[0] = 0.0
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-    st = ctx.stats(reset=True)
-    ms = e0.elapsed_time(e1) / args.steps if resident else (st["k1_ms"] + st["k2_ms"] + st["k3_ms"]) / args.steps
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        flags = torch.tensor([int(resident)], dtype=torch.int32, device=dev)
-        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
-        all_resident = bool(flags.item())
+        dist.barrier()
+    st = ctx.stats(reset=True)
+    mine_t = [e0.elapsed_time(e1) / steps, (st["k1_ms"] + st["k2_ms"] + st["k3_ms"]) / steps,
+              st["k1_ms"] / steps, 1000.0 * gather_s[0] / steps]
+    if world > 1:
+        t = torch.tensor(mine_t, dtype=torch.float64, device=dev)
+        allt = torch.empty(world * 4, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(allt, t)
+        allt = allt.view(world, 4).cpu().tolist()
     else:
-        all_resident = resident
-    if rank != 0:
-        dist.destroy_process_group()
-        return 0
+        allt = [mine_t]
+    wall = max(r[0] for r in allt)
+    kern = max(r[1] for r in allt)
     total_frames = sum(v.n for v in vids)
     total_bytes = sum(v.n * v.frame_bytes for v in vids)
     parity = None
-    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config.upper()}.json")
-    if os.path.exists(gpath) and out[1] is not None:
+    gpath = os.path.join(ROOT, "tests", "golden", f"{name.upper()}.json")
+    if rank == 0 and os.path.exists(gpath) and out[0] is not None:
         gold = {g["id"]: g for g in json.load(open(gpath))["videos"]}
-        got = {d["id"]: d for d in out[1]}
+        got = {d["id"]: d for d in out[0]}
         parity = len(got) == len(vids) and all(
             list(got[v.id]["detected"]) == gold[v.id]["detected"] and list(got[v.id]["final"]) == gold[v.id]["final"]
             for v in vids)
-    peak, peak_src = _peaks()
     k1_alg = sum(v.n * (v.frame_bytes + HIST_BYTES) for v in mine)
-    line = {
-        "metric": METRIC, "value": round(total_frames / (ms * 1e-3), 3), "unit": "frames/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic",
-        "config": {"workload": f"{args.config.upper()} (BASELINE.json configs)", "videos": len(vids),
-                   "lpt_imbalance_max_over_mean": round(max(sum(vids[i].n * vids[i].frame_bytes for i in a) for a in assign)
-                                                        / (sum(v.n * v.frame_bytes for v in vids) / world), 4),
-                   "frames": total_frames, "frame_bytes": total_bytes,
-                   "parallelism": f"LPT whole-video sharding over {world} GPU(s), one NCCL all-gather",
-                   "timing": "CUDA events around whole steps (frames resident)" if all_resident else
-                             "library CUDA events around K1+K2+K3 (frames streamed through the device "
-                             "generator callback; generation excluded) on at least one rank"},
-        "hbm_gbs": round(total_bytes / (ms * 1e-3) / 1e9, 1),
-        "frac_of_measured_hbm": round(total_bytes / (ms * 1e-3) / 1e9 / peak, 4),
-        "roofline": {"bound": "hbm", "achieved": round(k1_alg / (st["k1_ms"] / args.steps * 1e-3) / 1e9, 1),
-                     "peak": peak, "unit": "GB/s", "kernel": "k1_hist_kernel (rank 0)",
-                     "frac": round(k1_alg / (st["k1_ms"] / args.steps * 1e-3) / 1e9 / peak, 4)},
-        "gpu_launches": int(st["launches"]), "clocks": clk.summary(), "parity_vs_golden": parity,
+    del items
+    ctx.close()
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"{name.upper()} (BASELINE.json configs): {len(vids)} videos, {total_frames} frames, "
+                    f"{total_bytes / 1e9:.1f} GB",
+        "frames": total_frames, "frame_bytes": total_bytes, "videos": len(vids),
+        "value_wall": round(total_frames / (wall * 1e-3), 3),
+        "value_kernel": round(total_frames / (kern * 1e-3), 3),
+        "unit": "frames/s", "scaling": "strong",
+        "wall_ms_per_step": round(wall, 4), "kernel_ms_per_step": round(kern, 4),
+        "per_rank_wall_ms": [round(r[0], 4) for r in allt],
+        "per_rank_k1_ms": [round(r[2], 4) for r in allt],
+        "gather_wall_ms_per_step": [round(r[3], 4) for r in allt] if world > 1 else None,
+        "frames_source": "resident in HBM" if resident else
+                         "streamed at every rank: device generator fills the staging buffer per chunk "
+                         "(inside the wall clock, outside the kernel clock)",
+        "lpt_imbalance_max_over_mean": round(max(share) / (sum(share) / world), 4),
+        "k1_gbs_rank0": round(k1_alg / (mine_t[2] * 1e-3) / 1e9, 1) if mine_t[2] > 0 else None,
+        "parity_vs_golden": parity, "steps": steps, "warmup": warmup, "clocks": clk.summary(),
+        "gpu_launches_rank0": int(st["launches"]),
     }
-    print(json.dumps(line), flush=True)
+
+
+def run_config(args):
+    """--config C3|C4|C5: strong scaling of the config's fixed batch (time_batch)."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    synth.build(device=True)
+    b = time_batch(args.config, world, rank, dev, local, args.steps, args.warmup,
+                   resident_gb=args.resident_gb, force_stream=args.stream_frames,
+                   max_videos=args.max_videos)
+    if rank == 0:
+        peak, _ = _peaks()
+        ms = b["wall_ms_per_step"]
+        line = {
+            "metric": METRIC, "value": b["value_wall"], "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": b["workload"], "frames_source": b["frames_source"],
+                       "parallelism": f"LPT whole-video sharding over {world} GPU(s), one NCCL all-gather",
+                       "timing": "value = CUDA events around whole steps (max over ranks); "
+                                 "value_kernel = library events around K1+K2+K3"},
+            "hbm_gbs": round(b["frame_bytes"] / (ms * 1e-3) / 1e9, 1),
+            "frac_of_measured_hbm": round(b["frame_bytes"] / (ms * 1e-3) / 1e9 / peak, 4),
+            "batch": b, "gpu_launches": b["gpu_launches_rank0"], "clocks": b["clocks"],
+            "parity_vs_golden": b["parity_vs_golden"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def k1_noise(dev, stream, n: int = 1500):
+    """K1 on uniform-random-colour 1080p frames (C3 shape; every pixel its own
+    code: the worst case for the shared-memory atomics and hue-table banks,
+    SURVEY.md §8(d) "never quote only the friendly content")."""
+    import torch
+
+    from synth import manifest, torch_dev
+    from paper_2503_12964_b200 import Ctx
+    v = manifest.noise_video(0, 1920, 1080, n)
+    table = torch_dev.frame_table(v, dev)
+    frames = torch.empty((v.n, v.H, v.W, 3), dtype=torch.uint8, device=dev)
+    torch_dev.gen_frames(v, table, frames)
+    hist = torch.empty((v.n, 162), dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    ctx = Ctx(device=dev.index, stream=stream, timing=True)
+    with torch.cuda.stream(stream):
+        ctx.frame_scores(frames, hist=hist, want_l1=False, want_score=False)
+        torch.cuda.synchronize()
+        ctx.stats(reset=True)
+        for _ in range(3):
+            ctx.frame_scores(frames, hist=hist, want_l1=False, want_score=False)
+    torch.cuda.synchronize()
+    st = ctx.stats(reset=True)
+    ms = st["k1_ms"] / 3
+    alg = v.n * (v.frame_bytes + HIST_BYTES)
+    ctx.close()
+    del frames, hist
+    torch.cuda.empty_cache()
+    peak, _ = _peaks()
+    return {"workload": f"uniform-noise frames {v.W}x{v.H} x {v.n} ({v.n * v.frame_bytes / 1e9:.1f} GB, resident)",
+            "kernel": "k1_hist_kernel", "launch_ms": round(ms, 4),
+            "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "unit": "GB/s", "peak": peak,
+            "frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4), "frac_of_8tbs": round(alg / (ms * 1e-3) / 8e12, 4)}
 
 
 # ---------------------------------------------------------------- one video split by frames (f2)
@@ -712,7 +824,26 @@ def main():
     ap.add_argument("--resident-gb", type=float, default=150.0)
     ap.add_argument("--shard-frames", action="store_true",
                     help="split the C2 video by frame ranges over the GPUs (strong scaling)")
+    ap.add_argument("--stream-frames", action="store_true",
+                    help="--config: stream frames through the device generator at every N")
+    ap.add_argument("--no-noise", action="store_true", help="skip the uniform-noise K1 figure")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 strong-scaling figure")
+    ap.add_argument("--c3-steps", type=int, default=2)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # self-launch: one process per GPU under torch.distributed.run (NCCL)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.config:

@@ -44,7 +44,7 @@ struct clip_ctx {
   DevBuf segs, segs2, flags, vids, hist, l1, cand_slots, cand_count, cuts, ncuts, ncand, final_cuts, nfinal,
       detcos, pack, pack_cos, sink;
   DevBuf m_video, m_clip_video, m_f0, m_f1, m_piece_base, m_P, m_S, m_alive, m_alive2, m_cos_b,
-      m_cos_clip, m_counters, m_vstate, m_valive;
+      m_cos_clip, m_norm2, m_runs, m_counters, m_vstate, m_valive;
   DevBuf staging[2];
   cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
   // timing
@@ -321,7 +321,9 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   CKS(ensure(ctx, ctx->m_alive2, 4 * K));
   CKS(ensure(ctx, ctx->m_cos_b, 8 * K));
   CKS(ensure(ctx, ctx->m_cos_clip, 8 * K));
-  CKS(ensure(ctx, ctx->m_counters, 8 * 4));
+  CKS(ensure(ctx, ctx->m_norm2, 8 * K));
+  CKS(ensure(ctx, ctx->m_runs, 3 * 4 * K));
+  CKS(ensure(ctx, ctx->m_counters, 8 * 8));
   CKS(ensure(ctx, ctx->m_vstate, 8 * 4 * nv));
   CKS(ensure(ctx, ctx->m_valive, 8 * nv));
   CKS(ensure_pinned(ctx, std::max<size_t>(64, 8 * 4 * (size_t)nv)));
@@ -339,6 +341,10 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   s.alive2 = P<int32_t>(ctx->m_alive2);
   s.cos_b = P<double>(ctx->m_cos_b);
   s.cos_clip = P<double>(ctx->m_cos_clip);
+  s.norm2 = P<double>(ctx->m_norm2);
+  s.run_dest = P<int32_t>(ctx->m_runs);
+  s.run_lo = s.run_dest + K;
+  s.run_hi = s.run_lo + K;
   s.counters = P<int64_t>(ctx->m_counters);
   s.vstate = P<int64_t>(ctx->m_vstate);
   s.valive = P<int64_t>(ctx->m_valive);
@@ -350,23 +356,12 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
                          ctx->p.emb_stride > 1 ? (int32_t)ctx->p.emb_stride : 1, s, ctx->stream));
   CK(k3_clip_sum_launch((int32_t)K, dim, s, ctx->stream));
   ctx->stats.launches += 4;
-  int64_t n_alive = K - nv;
-  uint32_t r = 0;
-  while (n_alive > 0 && (ctx->p.max_merge_rounds == 0 || r < ctx->p.max_merge_rounds)) {
-    CK(k3_round_launch(d_mv, nv, dim, n_alive, ctx->p.merge_cos_threshold, ctx->p.band_rel, s,
-                       ctx->stream));
-    ctx->stats.launches += 2;
-    CK(cudaMemcpyAsync(ctx->hpin, s.counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->stats.memcpy_d2h += 16;
-    const int64_t* cnt = reinterpret_cast<const int64_t*>(ctx->hpin);
-    n_alive = cnt[0];
-    const int64_t merges = cnt[1];
-    std::swap(s.alive, s.alive2);
-    ++r;
-    if (merges == 0) break;
+  if (K - nv > 0) {
+    CK(k3_rounds_launch(d_mv, nv, dim, K - nv, ctx->p.merge_cos_threshold, ctx->p.band_rel,
+                        (int32_t)ctx->p.max_merge_rounds, ctx->sm_count, s, ctx->stream));
+    ctx->stats.launches += 1;
   }
-  CK(k3_finish_launch(d_mv, nv, (int32_t)K, n_alive, s, d_final, d_nfinal, d_detcos, ctx->stream));
+  CK(k3_finish_launch(d_mv, nv, (int32_t)K, s, d_final, d_nfinal, d_detcos, ctx->stream));
   ctx->stats.launches += 1;
   sp.end();
   CK(cudaMemcpyAsync(ctx->hpin, s.vstate, 8 * 4 * nv, cudaMemcpyDeviceToHost, ctx->stream));
@@ -463,7 +458,8 @@ int clip_detect_destroy(clip_ctx* ctx) {
                     &ctx->nfinal, &ctx->detcos, &ctx->pack, &ctx->pack_cos, &ctx->sink,
                     &ctx->m_video, &ctx->m_clip_video, &ctx->m_f0, &ctx->m_f1,
                     &ctx->m_piece_base, &ctx->m_P, &ctx->m_S, &ctx->m_alive, &ctx->m_alive2,
-                    &ctx->m_cos_b, &ctx->m_cos_clip, &ctx->m_counters, &ctx->m_vstate,
+                    &ctx->m_cos_b, &ctx->m_cos_clip, &ctx->m_norm2, &ctx->m_runs,
+                    &ctx->m_counters, &ctx->m_vstate,
                     &ctx->m_valive, &ctx->staging[0], &ctx->staging[1]};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);

@@ -94,7 +94,11 @@ struct MergeScratch {
   int32_t* alive2;      // [K]
   double* cos_b;        // [K]  per alive boundary
   double* cos_clip;     // [K]  per right-clip: cosine at its last evaluation
-  int64_t* counters;    // [4]  n_alive, merges this round, -, -
+  double* norm2;        // [K]  |S|^2 of the range starting at clip k
+  int32_t* run_dest;    // [K]  per run of merged boundaries: the range it joins
+  int32_t* run_lo;      // [K]  first merged boundary of the run (alive index)
+  int32_t* run_hi;      // [K]  one past the last
+  int64_t* counters;    // [8]  n_alive, merges this round, runs, -, next n_alive
   int64_t* vstate;      // [nv][4] done, rounds, band hits, merges this round (+ alive via vstate2)
   int64_t* valive;      // [nv] alive boundaries of the video after the round
 };
@@ -106,14 +110,16 @@ cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, i
                                 int64_t pieces_bound, int32_t stride, MergeScratch s,
                                 cudaStream_t stream);
 cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStream_t stream);
-// one merge round: cosines of the alive boundaries, decisions, ordered
-// compaction alive -> alive2 (the caller swaps the two pointers afterwards).
-cudaError_t k3_round_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t n_alive,
-                            double theta, double band_rel, MergeScratch s, cudaStream_t stream);
+// every merge round of every video on the device (one cooperative launch; the
+// alive list ends in s.alive, its length in s.counters[0]); max_alive bounds
+// the boundaries (grid size); max_rounds 0 = until the fixed point.
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
+                             double theta, double band_rel, int32_t max_rounds, int sm_count,
+                             MergeScratch s, cudaStream_t stream);
 // final cuts per video at cuts-array layout (offset cut_base, count n_final[v])
 // and the per-detected-cut cosines (same layout), from the alive list.
-cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int64_t n_alive,
-                             MergeScratch s, int32_t* final_cuts, int32_t* n_final,
-                             double* detected_cos, cudaStream_t stream);
+cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, MergeScratch s,
+                             int32_t* final_cuts, int32_t* n_final, double* detected_cos,
+                             cudaStream_t stream);
 
 }  // namespace clipdetect

@@ -10,10 +10,17 @@
 //  together".)
 //
 // Determinism: every sum runs in a fixed order (frames ascending inside a
-// <=16-frame piece, pieces ascending inside a clip, clips ascending inside a
-// merged range, fixed shuffle trees for the dot products); no float atomics.
-// The oracle sums a merged clip frame by frame, the device piece by piece:
+// <=16-frame piece, pieces ascending inside a clip; a merged range's sum is
+// the previous round's range sums added in ascending order; fixed shuffle
+// trees for the dot products and norms); no float atomics.  The oracle sums a
+// merged clip frame by frame, the device piece by piece and range by range:
 // same terms, different association (~1e-16 relative).
+//
+// The rounds run on the device (k3_rounds_kernel, one cooperative launch, grid
+// syncs between the phases): no host round trip per round, and a merged
+// range's sum and squared norm are kept, so a round costs O(D) per alive
+// boundary plus O(D) per absorbed range — not O(clips in range x D).
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "kernels.cuh"
@@ -56,7 +63,7 @@ __global__ void k3_clip_table_kernel(const MergeVideo* __restrict__ mv, int32_t 
   s.clip_f1[k] = j == m.n_clips - 1 ? (int32_t)m.n : cuts[m.cut_base + j];
 }
 
-// Block-wide exclusive scan helper (1024 threads).
+// Block-wide exclusive scan helper (any multiple of 32 threads up to 1024).
 __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* wsum, int32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t inc = x;
@@ -67,7 +74,7 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* wsum, int
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    int32_t w = wsum[lane];
+    int32_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
     int32_t wi = w;
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
@@ -111,6 +118,8 @@ k3_scan_kernel(int32_t K, MergeScratch s) {
     s.piece_base[K] = carry_p;
     s.counters[0] = carry_a;
     s.counters[1] = 0;
+    s.counters[2] = 0;
+    s.counters[3] = 0;
   }
 }
 
@@ -168,117 +177,193 @@ k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, i
   }
 }
 
-// S[k][d] = sum over the clip's pieces, ascending
+// S[k][d] = sum over the clip's pieces, ascending; norm2[k] = |S_k|^2
 __global__ void __launch_bounds__(kT)
 k3_clip_sum_kernel(int32_t dim, MergeScratch s) {
+  __shared__ double red[kT / 32];
   const int32_t k = blockIdx.x;
   const int32_t p0 = s.piece_base[k], p1 = s.piece_base[k + 1];
+  double n2 = 0.0;
   for (int32_t d = threadIdx.x; d < dim; d += kT) {
     double acc = 0.0;
     for (int32_t p = p0; p < p1; ++p) acc += s.P[(int64_t)p * dim + d];
     s.S[(int64_t)k * dim + d] = acc;
+    n2 += acc * acc;
   }
-}
-
-__device__ __forceinline__ double block_sum(double x, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  if (lane == 0) red[warp] = x;
+  for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  if (lane == 0) red[warp] = n2;
   __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    double t = 0.0;
     for (int w = 0; w < kT / 32; ++w) t += red[w];
-  __syncthreads();
-  return t;  // valid in thread 0
+    s.norm2[k] = t;
+  }
 }
 
-// cosine of every alive boundary b (left range | right range of clips)
+// Left range start of alive boundary b (the previous boundary of the same
+// video, else the video's first clip).
+__device__ __forceinline__ int32_t left_start(const MergeVideo* __restrict__ mv, const int32_t* alive,
+                                              const int32_t* clip_video, int64_t b, int32_t v) {
+  return (b > 0 && clip_video[alive[b - 1]] == v) ? alive[b - 1] : mv[v].clip_base;
+}
+
+// All merge rounds of every video in one cooperative launch.  Range sums live
+// in S at the range's first clip (S[k] = clip sum before any merge), their
+// squared norms in norm2.  Per round:
+//   1. cosines of the alive boundaries of videos not done: one warp per
+//      boundary, c = dot / (sqrt(|L|^2) sqrt(|R|^2)) (0 if a norm is 0);
+//   2. block 0: decisions (c >= theta merges, band hits |c - theta| <=
+//      band_rel * theta counted every evaluation), ordered compaction of the
+//      kept boundaries, the runs of merged boundaries (each run is added into
+//      the range on its left), per-video rounds / done flags;
+//   3. every run: S[dest] += S[absorbed ranges] ascending, then norm2[dest].
 __global__ void __launch_bounds__(kT)
-k3_cos_kernel(const MergeVideo* __restrict__ mv, int64_t n_alive, int32_t dim, MergeScratch s) {
-  __shared__ double red[kT / 32];
-  const int64_t b = blockIdx.x;
-  const int32_t rk = s.alive[b];
-  const int32_t v = s.clip_video[rk];
-  if (s.vstate[4 * v + VS_DONE]) return;
-  const int32_t lk0 = (b > 0 && s.clip_video[s.alive[b - 1]] == v) ? s.alive[b - 1] : mv[v].clip_base;
-  const int32_t rk1 = (b + 1 < n_alive && s.clip_video[s.alive[b + 1]] == v)
-                          ? s.alive[b + 1]
-                          : mv[v].clip_base + mv[v].n_clips;
-  double dot = 0.0, na = 0.0, nb = 0.0;
-  for (int32_t d = threadIdx.x; d < dim; d += kT) {
-    double L = 0.0, R = 0.0;
-    for (int32_t k = lk0; k < rk; ++k) L += s.S[(int64_t)k * dim + d];
-    for (int32_t k = rk; k < rk1; ++k) R += s.S[(int64_t)k * dim + d];
-    dot += L * R;
-    na += L * L;
-    nb += R * R;
-  }
-  dot = block_sum(dot, red);
-  na = block_sum(na, red);
-  nb = block_sum(nb, red);
-  if (threadIdx.x == 0) {
-    const double sa = sqrt(na), sb = sqrt(nb);
-    s.cos_b[b] = (sa == 0.0 || sb == 0.0) ? 0.0 : dot / (sa * sb);
-  }
-}
-
-// decisions + ordered compaction alive -> alive2 + per-video round bookkeeping
-__global__ void __launch_bounds__(1024)
-k3_decide_kernel(int32_t nv, int64_t n_alive, double theta, double band_rel, MergeScratch s) {
+k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, double theta,
+                 double band_rel, int32_t max_rounds, MergeScratch s) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   __shared__ int32_t wsum[33];
-  int32_t carry = 0;
-  int64_t merges = 0;
-  for (int32_t v = threadIdx.x; v < nv; v += 1024) s.valive[v] = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < n_alive; base += 1024) {
-    const int64_t b = base + threadIdx.x;
-    int32_t keep = 0, rk = 0;
-    if (b < n_alive) {
-      rk = s.alive[b];
-      const int32_t v = s.clip_video[rk];
-      keep = 1;
-      if (!s.vstate[4 * v + VS_DONE]) {
-        const double c = s.cos_b[b];
-        s.cos_clip[rk] = c;
-        if (fabs(c - theta) <= band_rel * theta)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_BAND]), 1ull);
-        if (c >= theta) {
-          keep = 0;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_MERGES]), 1ull);
-        }
-      }
-      if (keep) atomicAdd(reinterpret_cast<unsigned long long*>(&s.valive[v]), 1ull);
-    }
-    int32_t tot;
-    const int32_t e = block_excl_scan(keep, wsum, tot);
-    if (keep) s.alive2[carry + e] = rk;
-    carry += tot;
-  }
-  __syncthreads();
-  for (int32_t v = threadIdx.x; v < nv; v += 1024) {
-    int64_t* vs = s.vstate + 4 * v;
-    if (vs[VS_DONE]) continue;
-    vs[VS_ROUNDS] += 1;
-    merges += vs[VS_MERGES];
-    if (vs[VS_MERGES] == 0 || s.valive[v] == 0) vs[VS_DONE] = 1;
-    vs[VS_MERGES] = 0;
-  }
-  // reduce merges over threads
+  __shared__ double red[kT / 32];
   __shared__ unsigned long long m_tot;
-  if (threadIdx.x == 0) m_tot = 0;
-  __syncthreads();
-  if (merges) atomicAdd(&m_tot, (unsigned long long)merges);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s.counters[0] = carry;
-    s.counters[1] = (int64_t)m_tot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gwarp = (int64_t)blockIdx.x * (kT / 32) + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * (kT / 32);
+  int32_t* alive = s.alive;
+  int32_t* alive2 = s.alive2;
+  for (int32_t r = 0; max_rounds <= 0 || r < max_rounds; ++r) {
+    const int64_t n_alive = *(volatile int64_t*)&s.counters[0];
+    if (n_alive == 0) break;
+    // ---- 1. cosines
+    for (int64_t b = gwarp; b < n_alive; b += nwarps) {
+      const int32_t rk = alive[b];
+      const int32_t v = s.clip_video[rk];
+      if (s.vstate[4 * v + VS_DONE]) continue;
+      const int32_t lk = left_start(mv, alive, s.clip_video, b, v);
+      const double* __restrict__ L = s.S + (int64_t)lk * dim;
+      const double* __restrict__ R = s.S + (int64_t)rk * dim;
+      double dot = 0.0;
+      for (int32_t d = lane; d < dim; d += 32) dot += L[d] * R[d];
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (lane == 0) {
+        const double sa = sqrt(s.norm2[lk]), sb = sqrt(s.norm2[rk]);
+        s.cos_b[b] = (sa == 0.0 || sb == 0.0) ? 0.0 : dot / (sa * sb);
+      }
+    }
+    grid.sync();
+    // ---- 2. decisions, compaction, runs (block 0)
+    if (blockIdx.x == 0) {
+      for (int32_t v = threadIdx.x; v < nv; v += kT) s.valive[v] = 0;
+      if (threadIdx.x == 0) m_tot = 0;
+      __syncthreads();
+      int32_t carry = 0, rcarry = 0;
+      for (int64_t base = 0; base < n_alive; base += kT) {
+        const int64_t b = base + threadIdx.x;
+        int32_t keep = 0, rk = 0, run0 = 0, v = -1;
+        bool merged = false;
+        if (b < n_alive) {
+          rk = alive[b];
+          v = s.clip_video[rk];
+          keep = 1;
+          if (!s.vstate[4 * v + VS_DONE]) {
+            const double c = s.cos_b[b];
+            s.cos_clip[rk] = c;
+            if (fabs(c - theta) <= band_rel * theta)
+              atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_BAND]), 1ull);
+            if (c >= theta) {
+              keep = 0;
+              merged = true;
+              atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_MERGES]), 1ull);
+              atomicAdd(&m_tot, 1ull);
+            }
+          }
+          if (keep) atomicAdd(reinterpret_cast<unsigned long long*>(&s.valive[v]), 1ull);
+        }
+        __syncthreads();  // decisions of this chunk visible (cos_b of b - 1 may be in it)
+        if (merged) {
+          // a run of merged boundaries starts at b unless b - 1 (same video) merged too
+          bool prev_merged = false;
+          if (b > 0) {
+            const int32_t pk = alive[b - 1];
+            prev_merged = s.clip_video[pk] == v && !s.vstate[4 * v + VS_DONE] && s.cos_b[b - 1] >= theta;
+          }
+          run0 = !prev_merged;
+        }
+        int32_t tot, rtot;
+        const int32_t e = block_excl_scan(keep, wsum, tot);
+        const int32_t re = block_excl_scan(run0, wsum, rtot);
+        if (keep) alive2[carry + e] = rk;
+        if (run0) {
+          // run [b, j): merged boundaries of video v, added into the range on the left
+          int64_t j = b + 1;
+          while (j < n_alive && s.clip_video[alive[j]] == v && s.cos_b[j] >= theta) ++j;
+          const int32_t slot = rcarry + re;
+          s.run_dest[slot] = left_start(mv, alive, s.clip_video, b, v);
+          s.run_lo[slot] = (int32_t)b;
+          s.run_hi[slot] = (int32_t)j;
+        }
+        carry += tot;
+        rcarry += rtot;
+      }
+      __syncthreads();
+      for (int32_t v = threadIdx.x; v < nv; v += kT) {
+        int64_t* vs = s.vstate + 4 * v;
+        if (vs[VS_DONE]) continue;
+        vs[VS_ROUNDS] += 1;
+        if (vs[VS_MERGES] == 0 || s.valive[v] == 0) vs[VS_DONE] = 1;
+        vs[VS_MERGES] = 0;
+      }
+      if (threadIdx.x == 0) {
+        s.counters[1] = (int64_t)m_tot;
+        s.counters[2] = rcarry;
+        s.counters[4] = carry;  // next round's n_alive (published after the sums)
+      }
+    }
+    grid.sync();
+    const int64_t merges = *(volatile int64_t*)&s.counters[1];
+    if (merges == 0) break;  // every block reads the same value
+    // ---- 3. merged range sums and norms
+    const int32_t nruns = (int32_t)*(volatile int64_t*)&s.counters[2];
+    for (int32_t q = blockIdx.x; q < nruns; q += gridDim.x) {
+      const int32_t dest = s.run_dest[q], lo = s.run_lo[q], hi = s.run_hi[q];
+      double* __restrict__ D = s.S + (int64_t)dest * dim;
+      double n2 = 0.0;
+      for (int32_t d = threadIdx.x; d < dim; d += kT) {
+        double acc = D[d];
+        for (int32_t t = lo; t < hi; ++t) acc += s.S[(int64_t)alive[t] * dim + d];
+        D[d] = acc;
+        n2 += acc * acc;
+      }
+      for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      if (lane == 0) red[warp] = n2;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kT / 32; ++w) t += red[w];
+        s.norm2[dest] = t;
+      }
+      __syncthreads();
+    }
+    int32_t* tmp = alive;
+    alive = alive2;
+    alive2 = tmp;
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.counters[0] = s.counters[4];
+    grid.sync();
+  }
+  // the final alive list is in s.alive for k3_finish_kernel
+  if (alive != s.alive) {
+    const int64_t n_alive = *(volatile int64_t*)&s.counters[0];
+    grid.sync();  // every block has read n_alive before anyone writes
+    for (int64_t b = (int64_t)blockIdx.x * kT + threadIdx.x; b < n_alive; b += (int64_t)gridDim.x * kT)
+      s.alive[b] = alive[b];
   }
 }
 
 __global__ void k3_finish_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K,
-                                 int64_t n_alive, MergeScratch s, int32_t* __restrict__ final_cuts,
+                                 MergeScratch s, int32_t* __restrict__ final_cuts,
                                  int32_t* __restrict__ n_final, double* __restrict__ detected_cos) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_alive = s.counters[0];
   if (i < n_alive) {
     const int32_t rk = s.alive[i];
     const int32_t v = s.clip_video[rk];
@@ -324,22 +409,32 @@ cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t k3_round_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t n_alive,
-                            double theta, double band_rel, MergeScratch s, cudaStream_t stream) {
-  if (n_alive > 0) k3_cos_kernel<<<(unsigned)n_alive, kT, 0, stream>>>(d_mv, n_alive, dim, s);
-  k3_decide_kernel<<<1, 1024, 0, stream>>>(nv, n_alive, theta, band_rel, s);
-  return cudaGetLastError();
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
+                             double theta, double band_rel, int32_t max_rounds, int sm_count,
+                             MergeScratch s, cudaStream_t stream) {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3_rounds_kernel, kT, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+  }
+  // enough warps for one boundary each (up to every co-resident block)
+  int64_t want = (max_alive + kT / 32 - 1) / (kT / 32);
+  int64_t grid = (int64_t)sm_count * occ;
+  if (want < grid) grid = want < 1 ? 1 : want;
+  void* args[] = {(void*)&d_mv, (void*)&nv, (void*)&dim, (void*)&theta, (void*)&band_rel,
+                  (void*)&max_rounds, (void*)&s};
+  return cudaLaunchCooperativeKernel((const void*)k3_rounds_kernel, dim3((unsigned)grid), dim3(kT),
+                                     args, 0, stream);
 }
 
-cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int64_t n_alive,
-                             MergeScratch s, int32_t* final_cuts, int32_t* n_final,
-                             double* detected_cos, cudaStream_t stream) {
+cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, MergeScratch s,
+                             int32_t* final_cuts, int32_t* n_final, double* detected_cos,
+                             cudaStream_t stream) {
   cudaMemsetAsync(n_final, 0, sizeof(int32_t) * nv, stream);
-  const int64_t n = n_alive > K ? n_alive : K;
-  if (n > 0)
-    k3_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_mv, nv, K, n_alive, s,
-                                                                       final_cuts, n_final,
-                                                                       detected_cos);
+  if (K > 0)
+    k3_finish_kernel<<<(unsigned)((K + 255) / 256), 256, 0, stream>>>(d_mv, nv, K, s, final_cuts,
+                                                                       n_final, detected_cos);
   return cudaGetLastError();
 }
 

@@ -80,10 +80,10 @@ def test_band_hits_run_videos(dev):
         L = 8  # min_clip_frames default; stretch each clip to 8 frames
         n_clips = len(cuts) + 1
         n = L * n_clips
-        emb = np.zeros((n, e.shape[1]), dtype=np.float32)
+        emb = np.zeros((n, 16), dtype=np.float32)  # one dim for the whole batch
         bounds = [0] + list(cuts) + [e.shape[0]]
         for k in range(n_clips):
-            emb[L * k:L * (k + 1)] = e[bounds[k]]  # every frame of clip k: its planted vector
+            emb[L * k:L * (k + 1), :e.shape[1]] = e[bounds[k]]  # every frame of clip k: its planted vector
         frames = np.zeros((n, 16, 16, 3), dtype=np.uint8)
         for k in range(n_clips):
             frames[L * k:L * (k + 1)] = (255, 0, 0) if k % 2 == 0 else (0, 0, 255)

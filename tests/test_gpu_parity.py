@@ -556,3 +556,61 @@ def test_k1_every_colour_frame(dev):
     want = np.bincount(oracle.bin_table(), minlength=162).astype(np.uint32)
     assert np.array_equal(_u32(hist)[0], want)
     c.close()
+
+
+# ------------------------------------------------------------------ K3 at scale
+def _walk_embeddings(n_clips, frames_per_clip, dim, seed, step_deg):
+    """Clip k's frames share the unit vector at angle phi_k, phi a random walk
+    with steps uniform in [-step_deg, step_deg]: adjacent cosines straddle
+    theta = 0.9 (25.8 degrees), so merges cascade over several rounds."""
+    rng = np.random.default_rng(seed)
+    phi = np.cumsum(rng.uniform(-step_deg, step_deg, n_clips)) * np.pi / 180
+    e = np.zeros((n_clips * frames_per_clip, dim), dtype=np.float32)
+    v = np.stack([np.cos(phi), np.sin(phi)], axis=1).astype(np.float32)
+    e[:, :2] = np.repeat(v, frames_per_clip, axis=0)
+    cuts = [frames_per_clip * (k + 1) for k in range(n_clips - 1)]
+    return e, cuts
+
+
+@pytest.mark.parametrize("n_clips,step", [(2000, 40.0), (20001, 45.0)])
+def test_merge_many_cuts_multi_round(ctx, dev, n_clips, step):
+    """Thousands of boundaries merging over several rounds (the device-side
+    round loop and the incremental range sums) against the oracle: final cuts,
+    rounds and band hits exact, cosines within 1e-5."""
+    e, cuts = _walk_embeddings(n_clips, 3, 8, n_clips, step)
+    ref = oracle.merge(e, cuts)
+    m, cos, hits, rounds = ctx.merge(torch.from_numpy(e).to(dev),
+                                     torch.tensor(cuts, dtype=torch.int32, device=dev))
+    assert ref.rounds >= 3, ref.rounds
+    assert list(m.cpu().numpy()) == list(ref.final)
+    assert rounds == ref.rounds and hits == ref.n_band_hits
+    np.testing.assert_allclose(cos.cpu().numpy(), ref.cos, rtol=COS_RTOL, atol=1e-12)
+
+
+def test_merge_20k_cuts_near_constant_under_5ms(ctx, dev):
+    """A near-constant 768-d video with 20,000 detected cuts (every boundary
+    merges): clip_merge (piece sums, clip sums, all rounds on the device,
+    final cuts) in < 5 ms, and the oracle's result (one clip)."""
+    rng = np.random.default_rng(3)
+    n = 2 * 20001
+    base = rng.standard_normal(768)
+    e = (base[None, :] + 0.01 * rng.standard_normal((n, 768))).astype(np.float32)
+    cuts = list(range(2, n, 2))
+    assert len(cuts) == 20000
+    ed = torch.from_numpy(e).to(dev)
+    cd = torch.tensor(cuts, dtype=torch.int32, device=dev)
+    times = []
+    for _ in range(6):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(ctx.stream)
+        m, cos, hits, rounds = ctx.merge(ed, cd)
+        t1.record(ctx.stream)
+        torch.cuda.synchronize()
+        times.append(t0.elapsed_time(t1))
+    ref = oracle.merge(e, cuts)
+    assert list(m.cpu().numpy()) == list(ref.final) == []
+    assert rounds == ref.rounds
+    ms = float(np.median(times[1:]))
+    print(f"clip_merge 20,000 cuts x 768: {ms:.3f} ms (median of 5)")
+    assert ms < 5.0, times
