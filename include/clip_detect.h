@@ -28,6 +28,9 @@
  *    base 16-byte aligned, H*W % 32 == 0.  NV12 is converted to RGB by reading
  *    O0 (BT.601 limited range, 20-bit fixed point = OpenCV COLOR_YUV2RGB_NV12)
  *    inside the histogram kernel; the RGB frame is never materialised.
+ *    H*W < 2^31 (L1 <= 2 H W is a u32); with CLIP_DIST_CORREL H*W <= 2^27
+ *    (its exact int64 sums reach nbins (H W)^2); larger frames are
+ *    CLIP_E_INVALID.
  *  - Only compute capability 10.0 (B200, sm_100a) is supported: any other
  *    device gives CLIP_E_ARCH.  There is no CPU fallback.
  *  - Results are deterministic: histograms, L1, cuts bit-identical for any
@@ -168,7 +171,9 @@ int clip_cuts(clip_ctx* ctx, const uint32_t* l1, int64_t n_frames, int64_t pixel
  *   n_band_hits  host out or NULL: #evaluations with |cos - theta| <= band_rel*theta
  *   rounds       host out or NULL: rounds that evaluated cosines
  * O8: clip embedding = f64 sum of its frames' embeddings; O9: round-synchronous
- * merge of every adjacent pair with cos >= theta, to a fixed point. */
+ * merge of every adjacent pair with cos >= theta, to a fixed point.  Every
+ * round runs on the device (one cooperative kernel launch); the call
+ * synchronises once, at the end. */
 int clip_merge(clip_ctx* ctx, const float* emb, int64_t n_frames, int32_t dim,
                const int32_t* cuts, int64_t n_cuts, int32_t* merged, int64_t* n_merged,
                double* boundary_cos, int64_t* n_band_hits, int32_t* rounds);

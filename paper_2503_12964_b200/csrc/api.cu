@@ -278,7 +278,11 @@ int validate_frames(clip_ctx* ctx, const void* frames, int64_t n, int32_t h, int
   if (((int64_t)h * w) % (format == CLIP_FORMAT_NV12 ? 32 : 16) != 0)
     return fail(ctx, CLIP_E_INVALID, "H*W = %lld is not a multiple of %d", (long long)h * w,
                 format == CLIP_FORMAT_NV12 ? 32 : 16);
-  if ((int64_t)h * w > (1ll << 31)) return fail(ctx, CLIP_E_INVALID, "frame too large");
+  // L1 <= 2 N is stored as u32 (O3): N < 2^31.  The correlation distance (O3')
+  // sums nbins * sum(h^2) <= 256 N^2 in int64: N <= 2^27 (8K frames are 2^25).
+  if ((int64_t)h * w >= (1ll << 31)) return fail(ctx, CLIP_E_INVALID, "frame too large (H*W >= 2^31)");
+  if (ctx && ctx->p.distance == CLIP_DIST_CORREL && (int64_t)h * w > (1ll << 27))
+    return fail(ctx, CLIP_E_INVALID, "correlation distance needs H*W <= 2^27");
   if (!frames && !allow_null) return fail(ctx, CLIP_E_INVALID, "frames is NULL");
   if (frames && ((uintptr_t)frames & 15)) return fail(ctx, CLIP_E_INVALID, "frames not 16-byte aligned");
   return CLIP_OK;
@@ -322,7 +326,7 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   CKS(ensure(ctx, ctx->m_cos_b, 8 * K));
   CKS(ensure(ctx, ctx->m_cos_clip, 8 * K));
   CKS(ensure(ctx, ctx->m_norm2, 8 * K));
-  CKS(ensure(ctx, ctx->m_runs, 3 * 4 * K));
+  CKS(ensure(ctx, ctx->m_runs, 4 * (4 * K + 1)));
   CKS(ensure(ctx, ctx->m_counters, 8 * 8));
   CKS(ensure(ctx, ctx->m_vstate, 8 * 4 * nv));
   CKS(ensure(ctx, ctx->m_valive, 8 * nv));
@@ -345,6 +349,7 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   s.run_dest = P<int32_t>(ctx->m_runs);
   s.run_lo = s.run_dest + K;
   s.run_hi = s.run_lo + K;
+  s.run_cbase = s.run_hi + K;
   s.counters = P<int64_t>(ctx->m_counters);
   s.vstate = P<int64_t>(ctx->m_vstate);
   s.valive = P<int64_t>(ctx->m_valive);
@@ -541,7 +546,8 @@ int clip_frame_scores_nv12(clip_ctx* ctx, const uint8_t* frames, int64_t n_frame
 int clip_hist_scores(clip_ctx* ctx, const uint32_t* hist, int64_t n_frames, int64_t pixels_per_frame,
                      const uint32_t* prev_hist, uint32_t* l1, float* score) {
   CKS(check_ctx(ctx));
-  if (!hist || n_frames < 1 || pixels_per_frame < 1)
+  if (!hist || n_frames < 1 || pixels_per_frame < 1 || pixels_per_frame >= (1ll << 31) ||
+      (ctx->p.distance == CLIP_DIST_CORREL && pixels_per_frame > (1ll << 27)))
     return fail(ctx, CLIP_E_INVALID, "bad histograms (n %lld, N %lld)", (long long)n_frames,
                 (long long)pixels_per_frame);
   const uint32_t nbins = nbins_of(ctx->p);

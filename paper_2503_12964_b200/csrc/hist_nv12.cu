@@ -191,7 +191,10 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
   NvIter it;
   it.seek(segs, nseg, s_begin);
   // per-step increments of the (block row, 8-column chunk) position
-  int32_t cur_seg = -1, wu = 1, dq = 0, dr = 0;
+  int32_t cur_seg = -1, wu = 1, dq = 0, dr = 0, q64 = 0, r64 = 0, q640 = 0, r640 = 0;
+  // this stage's virtual lane u0 = (tid + 64 i) mod 640 and its (block row,
+  // 8-column chunk) = divmod(u0, wu), advanced incrementally (no per-stage division)
+  int32_t u0 = tid, br0 = 0, cx0 = 0;
   uint32_t slot = 0, par = 0;
   for (int32_t i = 0; i < n; ++i) {
     if (it.seg != cur_seg) {
@@ -199,14 +202,19 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
       wu = it.W >> 3;
       dq = kNvConsumers / wu;
       dr = kNvConsumers - dq * wu;
+      q64 = 64 / wu;
+      r64 = 64 - q64 * wu;
+      q640 = dq;
+      r640 = dr;
+      br0 = u0 / wu;
+      cx0 = u0 - br0 * wu;
     }
     const int32_t nr = it.nr(), W = it.W;
     mbar_wait(&sm.full[slot], par);
     const uint8_t* buf = sm.buf[slot];
     const uint8_t* uvb = buf + 2 * nr * W;
     const int32_t nu = nr * wu;
-    int32_t u = (tid + 64 * (i % (kNvConsumers / 64))) % kNvConsumers;  // virtual lane of this stage
-    int32_t br = u / wu, cx = u - br * wu;
+    int32_t u = u0, br = br0, cx = cx0;
 #pragma unroll 1
     for (; u < nu; u += kNvConsumers) {
       const uint8_t* yp = buf + 2 * br * W + 8 * cx;
@@ -229,6 +237,23 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
     if (++slot == kNvStages) {
       slot = 0;
       par ^= 1u;
+    }
+    // rotate the lane -> tile map by 64 lanes: u0 += 64 (mod 640)
+    u0 += 64;
+    br0 += q64;
+    cx0 += r64;
+    if (cx0 >= wu) {
+      cx0 -= wu;
+      ++br0;
+    }
+    if (u0 >= kNvConsumers) {
+      u0 -= kNvConsumers;
+      br0 -= q640;
+      cx0 -= r640;
+      if (cx0 < 0) {
+        cx0 += wu;
+        --br0;
+      }
     }
     const int32_t seg_now = it.seg, frame_now = it.frame;
     const bool last = (i + 1 == n);

@@ -98,7 +98,8 @@ struct MergeScratch {
   int32_t* run_dest;    // [K]  per run of merged boundaries: the range it joins
   int32_t* run_lo;      // [K]  first merged boundary of the run (alive index)
   int32_t* run_hi;      // [K]  one past the last
-  int64_t* counters;    // [8]  n_alive, merges this round, runs, -, next n_alive
+  int32_t* run_cbase;   // [K+1] first partial-sum chunk of each run
+  int64_t* counters;    // [8]  n_alive, merges this round, runs, chunks, next n_alive
   int64_t* vstate;      // [nv][4] done, rounds, band hits, merges this round (+ alive via vstate2)
   int64_t* valive;      // [nv] alive boundaries of the video after the round
 };

@@ -215,9 +215,14 @@ __device__ __forceinline__ int32_t left_start(const MergeVideo* __restrict__ mv,
 //      boundary, c = dot / (sqrt(|L|^2) sqrt(|R|^2)) (0 if a norm is 0);
 //   2. block 0: decisions (c >= theta merges, band hits |c - theta| <=
 //      band_rel * theta counted every evaluation), ordered compaction of the
-//      kept boundaries, the runs of merged boundaries (each run is added into
-//      the range on its left), per-video rounds / done flags;
-//   3. every run: S[dest] += S[absorbed ranges] ascending, then norm2[dest].
+//      kept boundaries, the runs of merged boundaries (each run joins the
+//      range on its left) cut into chunks of <= kChunk absorbed ranges, and
+//      per-video rounds / done flags;
+//   3a. every chunk: partial = sum of its ranges, ascending (the first chunk
+//      of a run starts with the run's own range), into the scratch rows of P;
+//   3b. every run: S[dest] = sum of its chunks' partials, ascending; norm2.
+constexpr int kChunk = 64;
+
 __global__ void __launch_bounds__(kT)
 k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, double theta,
                  double band_rel, int32_t max_rounds, MergeScratch s) {
@@ -256,14 +261,17 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
       for (int32_t v = threadIdx.x; v < nv; v += kT) s.valive[v] = 0;
       if (threadIdx.x == 0) m_tot = 0;
       __syncthreads();
+      // merged(b): b evaluated this round (its video not done) and c >= theta
+      auto merged_at = [&](int64_t b, int32_t v) {
+        return s.clip_video[alive[b]] == v && s.cos_b[b] >= theta;
+      };
       int32_t carry = 0, rcarry = 0;
       for (int64_t base = 0; base < n_alive; base += kT) {
         const int64_t b = base + threadIdx.x;
-        int32_t keep = 0, rk = 0, run0 = 0, v = -1;
-        bool merged = false;
+        int32_t keep = 0, rk = 0, run0 = 0, runend = 0;
         if (b < n_alive) {
           rk = alive[b];
-          v = s.clip_video[rk];
+          const int32_t v = s.clip_video[rk];
           keep = 1;
           if (!s.vstate[4 * v + VS_DONE]) {
             const double c = s.cos_b[b];
@@ -272,40 +280,38 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
               atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_BAND]), 1ull);
             if (c >= theta) {
               keep = 0;
-              merged = true;
               atomicAdd(reinterpret_cast<unsigned long long*>(&s.vstate[4 * v + VS_MERGES]), 1ull);
               atomicAdd(&m_tot, 1ull);
+              // a run of merged boundaries of video v: [first, last]
+              run0 = !(b > 0 && merged_at(b - 1, v));
+              runend = !(b + 1 < n_alive && merged_at(b + 1, v));
             }
           }
           if (keep) atomicAdd(reinterpret_cast<unsigned long long*>(&s.valive[v]), 1ull);
-        }
-        __syncthreads();  // decisions of this chunk visible (cos_b of b - 1 may be in it)
-        if (merged) {
-          // a run of merged boundaries starts at b unless b - 1 (same video) merged too
-          bool prev_merged = false;
-          if (b > 0) {
-            const int32_t pk = alive[b - 1];
-            prev_merged = s.clip_video[pk] == v && !s.vstate[4 * v + VS_DONE] && s.cos_b[b - 1] >= theta;
-          }
-          run0 = !prev_merged;
         }
         int32_t tot, rtot;
         const int32_t e = block_excl_scan(keep, wsum, tot);
         const int32_t re = block_excl_scan(run0, wsum, rtot);
         if (keep) alive2[carry + e] = rk;
         if (run0) {
-          // run [b, j): merged boundaries of video v, added into the range on the left
-          int64_t j = b + 1;
-          while (j < n_alive && s.clip_video[alive[j]] == v && s.cos_b[j] >= theta) ++j;
-          const int32_t slot = rcarry + re;
-          s.run_dest[slot] = left_start(mv, alive, s.clip_video, b, v);
-          s.run_lo[slot] = (int32_t)b;
-          s.run_hi[slot] = (int32_t)j;
+          s.run_dest[rcarry + re] = left_start(mv, alive, s.clip_video, b, s.clip_video[rk]);
+          s.run_lo[rcarry + re] = (int32_t)b;
         }
+        if (runend) s.run_hi[rcarry + re + run0 - 1] = (int32_t)(b + 1);  // its run's number
         carry += tot;
         rcarry += rtot;
       }
       __syncthreads();
+      // chunk bases of the runs: run q has ceil((hi - lo) / kChunk) chunks
+      int32_t ccarry = 0;
+      for (int32_t base = 0; base < rcarry; base += kT) {
+        const int32_t q = base + threadIdx.x;
+        const int32_t nc = q < rcarry ? (s.run_hi[q] - s.run_lo[q] + kChunk - 1) / kChunk : 0;
+        int32_t tot;
+        const int32_t e = block_excl_scan(nc, wsum, tot);
+        if (q < rcarry) s.run_cbase[q] = ccarry + e;
+        ccarry += tot;
+      }
       for (int32_t v = threadIdx.x; v < nv; v += kT) {
         int64_t* vs = s.vstate + 4 * v;
         if (vs[VS_DONE]) continue;
@@ -314,23 +320,45 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
         vs[VS_MERGES] = 0;
       }
       if (threadIdx.x == 0) {
+        s.run_cbase[rcarry] = ccarry;
         s.counters[1] = (int64_t)m_tot;
         s.counters[2] = rcarry;
+        s.counters[3] = ccarry;
         s.counters[4] = carry;  // next round's n_alive (published after the sums)
       }
     }
     grid.sync();
     const int64_t merges = *(volatile int64_t*)&s.counters[1];
     if (merges == 0) break;  // every block reads the same value
-    // ---- 3. merged range sums and norms
     const int32_t nruns = (int32_t)*(volatile int64_t*)&s.counters[2];
+    const int32_t nchunks = (int32_t)*(volatile int64_t*)&s.counters[3];
+    // ---- 3a. chunk partial sums (rows of P: the piece sums are no longer needed)
+    for (int32_t w = blockIdx.x; w < nchunks; w += gridDim.x) {
+      int32_t lo = 0, hi = nruns - 1;  // run of chunk w: last run with cbase <= w
+      while (lo < hi) {
+        const int32_t m = (lo + hi + 1) >> 1;
+        if (s.run_cbase[m] <= w) lo = m; else hi = m - 1;
+      }
+      const int32_t q = lo, c = w - s.run_cbase[q];
+      const int32_t t0 = s.run_lo[q] + c * kChunk;
+      const int32_t t1 = min(s.run_hi[q], t0 + kChunk);
+      const double* __restrict__ own = c == 0 ? s.S + (int64_t)s.run_dest[q] * dim : nullptr;
+      double* __restrict__ out = s.P + (int64_t)w * dim;
+      for (int32_t d = threadIdx.x; d < dim; d += kT) {
+        double acc = own ? own[d] : 0.0;
+        for (int32_t t = t0; t < t1; ++t) acc += s.S[(int64_t)alive[t] * dim + d];
+        out[d] = acc;
+      }
+    }
+    grid.sync();
+    // ---- 3b. merged range sums and norms
     for (int32_t q = blockIdx.x; q < nruns; q += gridDim.x) {
-      const int32_t dest = s.run_dest[q], lo = s.run_lo[q], hi = s.run_hi[q];
+      const int32_t dest = s.run_dest[q], c0 = s.run_cbase[q], c1 = s.run_cbase[q + 1];
       double* __restrict__ D = s.S + (int64_t)dest * dim;
       double n2 = 0.0;
       for (int32_t d = threadIdx.x; d < dim; d += kT) {
-        double acc = D[d];
-        for (int32_t t = lo; t < hi; ++t) acc += s.S[(int64_t)alive[t] * dim + d];
+        double acc = s.P[(int64_t)c0 * dim + d];
+        for (int32_t c = c0 + 1; c < c1; ++c) acc += s.P[(int64_t)c * dim + d];
         D[d] = acc;
         n2 += acc * acc;
       }
@@ -353,7 +381,6 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
   // the final alive list is in s.alive for k3_finish_kernel
   if (alive != s.alive) {
     const int64_t n_alive = *(volatile int64_t*)&s.counters[0];
-    grid.sync();  // every block has read n_alive before anyone writes
     for (int64_t b = (int64_t)blockIdx.x * kT + threadIdx.x; b < n_alive; b += (int64_t)gridDim.x * kT)
       s.alive[b] = alive[b];
   }

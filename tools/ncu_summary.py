@@ -100,8 +100,32 @@ def full(path, alg_bytes=None):
     return out
 
 
+def traffic(path, kind, alg_bytes, pixels, out_path):
+    """profiles/<kind>_traffic.json from a --set full capture: DRAM bytes per
+    algorithmic byte and thread-instructions per pixel of the LAST launch of
+    the kind's kernel, tied to the kernel sources by bench.kernel_src_sha."""
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    kname = {"k1": "k1_hist_kernel", "k1_nv12": "k1_nv12_kernel"}[kind]
+    rows = [r for r in full(path, alg_bytes) if kname in r.get("kernel", "")]
+    r = rows[-1]
+    inst = float(r["smsp__inst_executed.sum"].split()[0])
+    d = {"dram_bytes_per_alg_byte": r["dram_bytes_per_alg_byte"],
+         "thread_instr_per_px": round(inst * 32 / pixels, 3),
+         "kernel": r["kernel"], "src_sha": bench.kernel_src_sha(kind),
+         "source": f"{path} (ncu --set full, last {kname} launch; {alg_bytes:.0f} algorithmic bytes, "
+                   f"{pixels:.0f} pixels)"}
+    with open(out_path, "w") as f:
+        json.dump(d, f, indent=1)
+    return d
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        print(json.dumps(traffic(sys.argv[2], sys.argv[3], float(sys.argv[4]), float(sys.argv[5]),
+                                 sys.argv[6]), indent=1))
+    elif sys.argv[1] == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     else:
         print(json.dumps(full(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None), indent=1))
