@@ -79,6 +79,7 @@ def _sharded(frames, emb, world, nv12=False):
     the concatenated histograms and the whole-video L1."""
     from paper_2503_12964_b200 import Ctx
     from paper_2503_12964_b200 import dist as cdist
+    torch.cuda.synchronize()  # inputs were made on the default stream; the ranks use their own
     n = frames.shape[0]
     shards = cdist.frame_shards(n, world)
     comm = ThreadComm(world)
