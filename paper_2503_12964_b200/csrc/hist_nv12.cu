@@ -49,8 +49,17 @@ constexpr int kNvLutBytes = 65536;
 static_assert(kNvConsumers % 64 == 0, "rotation by two warps");
 constexpr uint32_t kNvDynSmemBase = 0x400;  // see hist.cu kDynSmemBase
 
+// The stage in a ring slot, written by the producer before it arms the slot's
+// "full" barrier (see hist.cu StageMeta): the consumers run no iterator.
+struct NvMeta {
+  uint32_t* gh;  // the frame's global histogram, when this stage is its last; else null
+  int32_t nr;    // chroma-block rows in the stage
+  int32_t W;     // frame width
+};
+
 struct NvSmem {
   alignas(128) uint8_t buf[kNvStages][kNvStageBytes];
+  NvMeta meta[kNvStages];
   uint8_t lut[kNvLutBytes];  // lut[lut_index(na, d)] = lut_entry_dir(na, d, kHashNv12)
   uint32_t hist[kDirCodes];
   uint8_t c2b[kDirCodes];
@@ -67,8 +76,10 @@ struct NvIter {
   int32_t seg, frame, st;
   int32_t H, W, R, stages, n_frames;
   const uint8_t* frames;
+  uint32_t* hist;
   __device__ void load() {
     const Nv12Seg& g = segs[seg];
+    hist = g.hist;
     H = g.height;
     W = g.width;
     R = g.rows;
@@ -175,11 +186,8 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, uint32_t sb
 // tile map is rotated by 64 lanes (two warps) per stage so that the one-tile
 // warps move over the four schedulers instead of always being the same ones.
 template <int MODE, bool IMM>
-__device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Seg* segs,
-                                           int32_t nseg, int64_t s_begin, int32_t n,
-                                           uint32_t* sink) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  constexpr uint32_t nbins = 162;
+__device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, uint32_t* sink) {
+  const int tid = threadIdx.x;
   MadK mk;
   {
     const volatile uint32_t* v = reinterpret_cast<const volatile uint32_t*>(&sm.mk);
@@ -188,18 +196,18 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t xacc = 0;
-  NvIter it;
-  it.seek(segs, nseg, s_begin);
   // per-step increments of the (block row, 8-column chunk) position
-  int32_t cur_seg = -1, wu = 1, dq = 0, dr = 0, q64 = 0, r64 = 0, q640 = 0, r640 = 0;
+  int32_t cur_w = -1, wu = 1, dq = 0, dr = 0, q64 = 0, r64 = 0, q640 = 0, r640 = 0;
   // this stage's virtual lane u0 = (tid + 64 i) mod 640 and its (block row,
   // 8-column chunk) = divmod(u0, wu), advanced incrementally (no per-stage division)
   int32_t u0 = tid, br0 = 0, cx0 = 0;
   uint32_t slot = 0, par = 0;
   for (int32_t i = 0; i < n; ++i) {
-    if (it.seg != cur_seg) {
-      cur_seg = it.seg;
-      wu = it.W >> 3;
+    mbar_wait(&sm.full[slot], par);
+    const NvMeta meta = sm.meta[slot];
+    if (meta.W != cur_w) {
+      cur_w = meta.W;
+      wu = meta.W >> 3;
       dq = kNvConsumers / wu;
       dr = kNvConsumers - dq * wu;
       q64 = 64 / wu;
@@ -209,8 +217,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
       br0 = u0 / wu;
       cx0 = u0 - br0 * wu;
     }
-    const int32_t nr = it.nr(), W = it.W;
-    mbar_wait(&sm.full[slot], par);
+    const int32_t nr = meta.nr, W = meta.W;
     const uint8_t* buf = sm.buf[slot];
     const uint8_t* uvb = buf + 2 * nr * W;
     const int32_t nu = nr * wu;
@@ -232,8 +239,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
         ++br;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    mbar_arrive(&sm.empty[slot]);  // every consumer lane: its reads of the slot are done
     if (++slot == kNvStages) {
       slot = 0;
       par ^= 1u;
@@ -255,13 +261,10 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, const Nv12Se
         --br0;
       }
     }
-    const int32_t seg_now = it.seg, frame_now = it.frame;
-    const bool last = (i + 1 == n);
-    const bool changed = it.next(!last);
-    if (MODE == kModeFast && (last || changed)) {
+    if (MODE == kModeFast && meta.gh != nullptr) {
       // one RED per non-zero code to the frame's global bins (as K1)
       named_bar_sync(1, kNvConsumers);
-      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
+      uint32_t* gh = meta.gh;
       for (uint32_t cc = tid; cc < (uint32_t)kDirCodes; cc += kNvConsumers) {
         const uint32_t cnt = sm.hist[cc];
         if (cnt) {
@@ -300,7 +303,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kNvStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kNvWarps);
+      mbar_init(&sm.empty[i], kNvConsumers);
     }
     fence_mbar_init();
   }
@@ -317,15 +320,17 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       uint32_t slot = 0, par = 0;
       for (int32_t i = 0; i < n; ++i) {
         if (i >= kNvStages) mbar_wait(&sm.empty[slot], par ^ 1u);
-        const int32_t nr = it.nr();
-        const uint32_t ybytes = 2u * nr * it.W, cbytes = (uint32_t)nr * it.W;
-        const uint8_t* fb = it.frame_base();
-        const int64_t r0 = (int64_t)it.st * it.R;
-        mbar_arrive_expect_tx(&sm.full[slot], ybytes + cbytes);
-        bulk_g2s(sm.buf[slot], fb + 2 * r0 * it.W, ybytes, &sm.full[slot], pol);
-        bulk_g2s(sm.buf[slot] + ybytes, fb + (int64_t)it.H * it.W + r0 * it.W, cbytes,
-                 &sm.full[slot], pol);
-        it.next(i + 1 < n);
+        const int32_t nr = it.nr(), W = it.W;
+        const uint32_t ybytes = 2u * nr * W, cbytes = (uint32_t)nr * W;
+        const uint8_t* ysrc = it.frame_base() + 2 * (int64_t)it.st * it.R * W;
+        const uint8_t* csrc = it.frame_base() + (int64_t)it.H * W + (int64_t)it.st * it.R * W;
+        uint32_t* gh = it.hist + (int64_t)it.frame * 162;
+        const bool last = i + 1 == n;
+        const bool changed = it.next(!last);  // the frame ends with this stage
+        sm.meta[slot] = NvMeta{(last || changed) ? gh : nullptr, nr, W};
+        mbar_arrive_expect_tx(&sm.full[slot], ybytes + cbytes);  // release: orders the meta store
+        bulk_g2s(sm.buf[slot], ysrc, ybytes, &sm.full[slot], pol);
+        bulk_g2s(sm.buf[slot] + ybytes, csrc, cbytes, &sm.full[slot], pol);
         if (++slot == kNvStages) {
           slot = 0;
           par ^= 1u;
@@ -337,9 +342,9 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
   // ------------------------------------------------------------ consumers
   const uint32_t sb = smem_u32(smem_raw);
   if (sb == kNvDynSmemBase)
-    nv_consume<MODE, true>(sm, sb, segs, nseg, s_begin, n, sink);
+    nv_consume<MODE, true>(sm, sb, n, sink);
   else
-    nv_consume<MODE, false>(sm, sb, segs, nseg, s_begin, n, sink);
+    nv_consume<MODE, false>(sm, sb, n, sink);
 }
 
 // ------------------------------------------------------------ generic kernel
