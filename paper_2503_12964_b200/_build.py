@@ -25,14 +25,21 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Each source compiled to an object in parallel, then one shared-library link."""
-    if force or stale():
+CHECKED_LIB = os.path.join(HERE, "build_checked", "libclipdetect_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Each source compiled to an object in parallel, then one shared-library link.
+    checked: the bounds-checked build (-DCLIPDETECT_CHECKED, common.cuh CD_CHECK)
+    in build_checked/ — a test tool, never the product library."""
+    lib = CHECKED_LIB if checked else LIB
+    if force or not os.path.exists(lib) or any(os.path.getmtime(p) > os.path.getmtime(lib)
+                                               for p in _inputs()):
         from concurrent.futures import ThreadPoolExecutor
 
-        objdir = os.path.join(HERE, "build")
+        objdir = os.path.join(HERE, "build_checked" if checked else "build")
         os.makedirs(objdir, exist_ok=True)
-        cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+        cflags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DCLIPDETECT_CHECKED"] if checked else [])
         if verbose:
             cflags = ["-Xptxas=-v"] + cflags
 
@@ -45,5 +52,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
             objs = list(ex.map(compile_one, SOURCES))
         subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                               "-Xcompiler", "-fPIC", "-o", LIB, *objs], cwd=CSRC)
-    return LIB
+                               "-Xcompiler", "-fPIC", "-o", lib, *objs], cwd=CSRC)
+    return lib

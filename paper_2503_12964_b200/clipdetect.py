@@ -82,12 +82,16 @@ FORMAT_NV12 = 1
 _lib = None
 
 
-def load(build_if_missing: bool = False):
-    """Load libclipdetect.so (raises if it is missing: no fallback path)."""
+def load(build_if_missing: bool = False, path: str | None = None):
+    """Load libclipdetect.so (raises if it is missing: no fallback path).
+    ``path`` (before the first load only): another build of the same library,
+    e.g. the bounds-checked one of tools/sanitize_run.py."""
     global _lib
     if _lib is not None:
+        if path is not None and path != _lib._name:
+            raise RuntimeError(f"libclipdetect already loaded from {_lib._name}")
         return _lib
-    path = LIB_PATH
+    path = path or LIB_PATH
     if not os.path.exists(path):
         if build_if_missing:
             _build.build()

@@ -362,7 +362,7 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   CK(k3_clip_sum_launch((int32_t)K, dim, s, ctx->stream));
   ctx->stats.launches += 4;
   if (K - nv > 0) {
-    CK(k3_rounds_launch(d_mv, nv, dim, K - nv, ctx->p.merge_cos_threshold, ctx->p.band_rel,
+    CK(k3_rounds_launch(d_mv, nv, (int32_t)K, dim, K - nv, ctx->p.merge_cos_threshold, ctx->p.band_rel,
                         (int32_t)ctx->p.max_merge_rounds, ctx->sm_count, s, ctx->stream));
     ctx->stats.launches += 1;
   }

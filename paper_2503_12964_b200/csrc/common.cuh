@@ -4,10 +4,31 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace clipdetect {
 
 constexpr int kSMs = 148;
+
+// Checked build (-DCLIPDETECT_CHECKED, tools/sanitize_run.py --checked: the
+// pool's compute-sanitizer is closed): CD_CHECK(c) bounds-checks a shared- or
+// global-memory access, a ring hand-off or an index, prints the failing
+// condition and traps (the call then fails with CLIP_E_CUDA).  The product
+// build compiles every check away.
+#ifdef CLIPDETECT_CHECKED
+#define CD_CHECK(c)                                                                           \
+  do {                                                                                        \
+    if (!(c)) {                                                                               \
+      printf("CD_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,            \
+             (int)blockIdx.x, (int)threadIdx.x, #c);                                          \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define CD_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

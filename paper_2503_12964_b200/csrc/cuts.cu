@@ -11,6 +11,7 @@
 // Layout: one warp per frame for L1 (lanes stride the bins, redux.sync add),
 // candidate flags compacted IN ORDER per 128-frame block with ballot/popc,
 // then one warp per video walks the blocks' compacted lists in order.
+#include "common.cuh"
 #include "kernels.cuh"
 
 namespace clipdetect {
@@ -116,6 +117,7 @@ __global__ void k2_greedy_kernel(const VideoDesc* __restrict__ vids, int32_t nvi
   for (int64_t cb = c0; cb <= c1; cb += 32) {
     const int64_t c = cb + lane;
     const int32_t cnt = c <= c1 ? cand_count[c] : 0;
+    CD_CHECK(cnt >= 0 && cnt <= kCompactFrames);
     uint32_t nz = __ballot_sync(0xffffffffu, cnt > 0);
     while (nz) {
       const int src = __ffs(nz) - 1;
@@ -131,6 +133,7 @@ __global__ void k2_greedy_kernel(const VideoDesc* __restrict__ vids, int32_t nvi
           const int64_t t = f - fbase;
           ++nc;
           if (t - last >= l_min) {
+            CD_CHECK(k < n && t > last);  // cuts strictly increasing, capacity n per video
             if (lane == 0) out[k] = (int32_t)t;
             ++k;
             last = t;

@@ -58,7 +58,7 @@ constexpr uint32_t kDynSmemBase = 0x400;
 struct StageMeta {
   uint32_t* gh;   // the frame's global histogram, when this stage is its last; else null
   int32_t ng;     // 48-byte groups in the stage
-  int32_t pad;
+  int32_t seq;    // the stage's index in the CTA's range (checked builds verify the hand-off)
 };
 
 struct K1Smem {
@@ -175,6 +175,8 @@ __device__ __forceinline__ void bin_quads(const uint8_t* buf, int q0, int qstrid
   }
 #pragma unroll
   for (int j = 0; j < 2 * NQ; ++j) {
+    CD_CHECK(dir_off_lo(pre[j], qa[j]) < 4u * kDirCodes && (dir_off_lo(pre[j], qa[j]) & 3u) == 0);
+    CD_CHECK(dir_off_hi(pre[j], qb[j]) < 4u * kDirCodes && (dir_off_hi(pre[j], qb[j]) & 3u) == 0);
     hist_inc<IMM>(sb, dir_off_lo(pre[j], qa[j]));
     hist_inc<IMM>(sb, dir_off_hi(pre[j], qb[j]));
   }
@@ -216,9 +218,11 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, int32_t n
     mbar_wait(&sm.full[slot], par);
     const StageMeta meta = sm.meta[slot];
     const int ng = meta.ng;
+    CD_CHECK(meta.seq == i && ng >= 1 && ng <= kStageGroups);  // the slot holds stage i
     const uint8_t* buf = sm.buf[slot];
     if constexpr (MODE == kModeFast) {
       if (ng == kStageGroups) {
+        CD_CHECK((tid + (kQPL - 1) * kConsumers + 1) * 12 <= ng * 48);
         bin_quads<kQPL, IMM>(buf, tid, kConsumers, sbase, mk);
       } else {  // ragged last stage of a frame: quad by quad
         for (int q = tid; q < ng * 4; q += kConsumers) bin_quads<1, IMM>(buf, q, 0, sbase, mk);
@@ -244,6 +248,7 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, int32_t n
         const uint32_t cnt = sm.hist[c];
         if (cnt) {
           sm.hist[c] = 0u;
+          CD_CHECK((MODE == kModeFast ? sm.c2b[c] : c) < nbins);  // only reachable codes counted
           atomicAdd(meta.gh + (MODE == kModeFast ? sm.c2b[c] : c), cnt);
         }
       }
@@ -298,11 +303,13 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
         if (i >= kStages) mbar_wait(&sm.empty[slot], par ^ 1u);
         const int32_t ng = it.ng();
         const uint8_t* src = it.src();
+        const uint32_t bytes = (uint32_t)ng * 48u;
+        CD_CHECK(ng >= 1 && ng <= kStageGroups && (reinterpret_cast<uintptr_t>(src) & 15) == 0);
+        CD_CHECK(src >= it.frames && src + bytes <= it.frames + (int64_t)it.n_frames * it.groups * 48);
         uint32_t* gh = it.hist + (int64_t)it.frame * nbins;
         const bool last = i + 1 == n;
         const bool changed = it.next(!last);  // the frame ends with this stage
-        sm.meta[slot] = StageMeta{(last || changed) ? gh : nullptr, ng, 0};
-        const uint32_t bytes = (uint32_t)ng * 48u;
+        sm.meta[slot] = StageMeta{(last || changed) ? gh : nullptr, ng, i};
         mbar_arrive_expect_tx(&sm.full[slot], bytes);  // release: orders the meta store
         bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
         if (++slot == kStages) {

@@ -55,6 +55,8 @@ struct NvMeta {
   uint32_t* gh;  // the frame's global histogram, when this stage is its last; else null
   int32_t nr;    // chroma-block rows in the stage
   int32_t W;     // frame width
+  int32_t seq;   // the stage's index in the CTA's range (checked builds verify the hand-off)
+  int32_t pad;
 };
 
 struct NvSmem {
@@ -176,6 +178,7 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, uint32_t sb
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
+    CD_CHECK(dir_off_lo(pre[j], qa[j]) < 4u * kDirCodes && dir_off_hi(pre[j], qb[j]) < 4u * kDirCodes);
     nv_hist_inc<IMM>(sb, dir_off_lo(pre[j], qa[j]));
     nv_hist_inc<IMM>(sb, dir_off_hi(pre[j], qb[j]));
   }
@@ -205,6 +208,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
   for (int32_t i = 0; i < n; ++i) {
     mbar_wait(&sm.full[slot], par);
     const NvMeta meta = sm.meta[slot];
+    CD_CHECK(meta.seq == i && meta.nr >= 1 && (meta.W & 15) == 0);  // the slot holds stage i
     if (meta.W != cur_w) {
       cur_w = meta.W;
       wu = meta.W >> 3;
@@ -224,6 +228,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
     int32_t u = u0, br = br0, cx = cx0;
 #pragma unroll 1
     for (; u < nu; u += kNvConsumers) {
+      CD_CHECK(br < nr && cx < wu);  // the tile lies inside the stage's rows
       const uint8_t* yp = buf + 2 * br * W + 8 * cx;
       const uint2 a = *reinterpret_cast<const uint2*>(yp);
       const uint2 b = *reinterpret_cast<const uint2*>(yp + W);
@@ -269,6 +274,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
         const uint32_t cnt = sm.hist[cc];
         if (cnt) {
           sm.hist[cc] = 0u;
+          CD_CHECK(sm.c2b[cc] < 162);  // only reachable codes counted
           atomicAdd(gh + sm.c2b[cc], cnt);
         }
       }
@@ -324,10 +330,13 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
         const uint32_t ybytes = 2u * nr * W, cbytes = (uint32_t)nr * W;
         const uint8_t* ysrc = it.frame_base() + 2 * (int64_t)it.st * it.R * W;
         const uint8_t* csrc = it.frame_base() + (int64_t)it.H * W + (int64_t)it.st * it.R * W;
+        CD_CHECK(nr >= 1 && ybytes + cbytes <= kNvStageBytes && ((ybytes | cbytes) & 15) == 0);
+        CD_CHECK(ysrc >= it.frame_base() && csrc + cbytes <= it.frame_base() + 3 * (int64_t)it.H * W / 2);
+        CD_CHECK(it.frame < it.n_frames);
         uint32_t* gh = it.hist + (int64_t)it.frame * 162;
         const bool last = i + 1 == n;
         const bool changed = it.next(!last);  // the frame ends with this stage
-        sm.meta[slot] = NvMeta{(last || changed) ? gh : nullptr, nr, W};
+        sm.meta[slot] = NvMeta{(last || changed) ? gh : nullptr, nr, W, i, 0};
         mbar_arrive_expect_tx(&sm.full[slot], ybytes + cbytes);  // release: orders the meta store
         bulk_g2s(sm.buf[slot], ysrc, ybytes, &sm.full[slot], pol);
         bulk_g2s(sm.buf[slot] + ybytes, csrc, cbytes, &sm.full[slot], pol);

@@ -114,7 +114,7 @@ cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStrea
 // every merge round of every video on the device (one cooperative launch; the
 // alive list ends in s.alive, its length in s.counters[0]); max_alive bounds
 // the boundaries (grid size); max_rounds 0 = until the fixed point.
-cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim, int64_t max_alive,
                              double theta, double band_rel, int32_t max_rounds, int sm_count,
                              MergeScratch s, cudaStream_t stream);
 // final cuts per video at cuts-array layout (offset cut_base, count n_final[v])

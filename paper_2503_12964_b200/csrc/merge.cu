@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 #include <math.h>
 
+#include "common.cuh"
 #include "kernels.cuh"
 
 namespace clipdetect {
@@ -224,7 +225,7 @@ __device__ __forceinline__ int32_t left_start(const MergeVideo* __restrict__ mv,
 constexpr int kChunk = 64;
 
 __global__ void __launch_bounds__(kT)
-k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, double theta,
+k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K, int32_t dim, double theta,
                  double band_rel, int32_t max_rounds, MergeScratch s) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -239,9 +240,11 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
   for (int32_t r = 0; max_rounds <= 0 || r < max_rounds; ++r) {
     const int64_t n_alive = *(volatile int64_t*)&s.counters[0];
     if (n_alive == 0) break;
+    CD_CHECK(n_alive < K);
     // ---- 1. cosines
     for (int64_t b = gwarp; b < n_alive; b += nwarps) {
       const int32_t rk = alive[b];
+      CD_CHECK(rk > 0 && rk < K && (b == 0 || alive[b - 1] < rk));  // sorted right-clip indices
       const int32_t v = s.clip_video[rk];
       if (s.vstate[4 * v + VS_DONE]) continue;
       const int32_t lk = left_start(mv, alive, s.clip_video, b, v);
@@ -342,6 +345,7 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
       const int32_t q = lo, c = w - s.run_cbase[q];
       const int32_t t0 = s.run_lo[q] + c * kChunk;
       const int32_t t1 = min(s.run_hi[q], t0 + kChunk);
+      CD_CHECK(w < K && c >= 0 && t0 < t1 && t1 <= n_alive && s.run_dest[q] < alive[t0]);
       const double* __restrict__ own = c == 0 ? s.S + (int64_t)s.run_dest[q] * dim : nullptr;
       double* __restrict__ out = s.P + (int64_t)w * dim;
       for (int32_t d = threadIdx.x; d < dim; d += kT) {
@@ -354,6 +358,7 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, dou
     // ---- 3b. merged range sums and norms
     for (int32_t q = blockIdx.x; q < nruns; q += gridDim.x) {
       const int32_t dest = s.run_dest[q], c0 = s.run_cbase[q], c1 = s.run_cbase[q + 1];
+      CD_CHECK(dest >= 0 && dest < K && c0 < c1 && c1 <= nchunks);
       double* __restrict__ D = s.S + (int64_t)dest * dim;
       double n2 = 0.0;
       for (int32_t d = threadIdx.x; d < dim; d += kT) {
@@ -436,7 +441,7 @@ cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim, int64_t max_alive,
                              double theta, double band_rel, int32_t max_rounds, int sm_count,
                              MergeScratch s, cudaStream_t stream) {
   static int occ = 0;
@@ -449,8 +454,8 @@ cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, in
   int64_t want = (max_alive + kT / 32 - 1) / (kT / 32);
   int64_t grid = (int64_t)sm_count * occ;
   if (want < grid) grid = want < 1 ? 1 : want;
-  void* args[] = {(void*)&d_mv, (void*)&nv, (void*)&dim, (void*)&theta, (void*)&band_rel,
-                  (void*)&max_rounds, (void*)&s};
+  void* args[] = {(void*)&d_mv, (void*)&nv, (void*)&K, (void*)&dim, (void*)&theta,
+                  (void*)&band_rel, (void*)&max_rounds, (void*)&s};
   return cudaLaunchCooperativeKernel((const void*)k3_rounds_kernel, dim3((unsigned)grid), dim3(kT),
                                      args, 0, stream);
 }

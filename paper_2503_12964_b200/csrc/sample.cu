@@ -116,6 +116,9 @@ k4_sample_kernel(const uint8_t* __restrict__ frames, int64_t n, int32_t H, int32
                                      : fb + (int64_t)H * W + (int64_t)(sy >> 1) * W;  // UV row
       const uintptr_t a0 = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;
       const uintptr_t a1 = (reinterpret_cast<uintptr_t>(row) + row_bytes + 15) & ~(uintptr_t)15;
+      CD_CHECK(q < 64 && a1 - a0 <= (uintptr_t)slot_bytes && (int64_t)(q + 1) * slot_bytes <= 2LL * rb * slot_bytes * (NV12 ? 2 : 1));
+      CD_CHECK(a0 >= reinterpret_cast<uintptr_t>(frames) &&
+               a1 <= reinterpret_cast<uintptr_t>(frames) + (uintptr_t)n * (NV12 ? 3 * (uint64_t)H * W / 2 : 3 * (uint64_t)H * W));
       row_off[q] = (int32_t)(reinterpret_cast<uintptr_t>(row) - a0);
       mbar_expect_tx(&bar, (uint32_t)(a1 - a0));
       bulk_g2s(rows + (int64_t)q * slot_bytes, reinterpret_cast<const uint8_t*>(a0),

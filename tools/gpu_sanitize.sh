@@ -1,12 +1,11 @@
-# ONE compute-sanitizer tool per gpurun call (B200_PROFILING.md: several tools in one
-# call have left a GPU unusable).  usage: bash tools/gpu_sanitize.sh <tool> [c2_frames]
-TOOL=$1; N=${2:-200}
+# Memory / hand-off checking of every kernel of the path.  compute-sanitizer is closed on
+# this pool, so this runs tools/sanitize_run.py on the bounds-checked build of the library
+# (-DCLIPDETECT_CHECKED, common.cuh CD_CHECK) after the same run on the product build.
+# usage: bash tools/gpu_sanitize.sh [c2_frames]    (logs in gpurun_out/r2/sanitizer/)
+N=${1:-200}
 mkdir -p gpurun_out/r2/sanitizer
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 1200 python tools/sanitize_run.py $N > gpurun_out/r2/sanitizer/plain_$TOOL.log 2>&1
-echo "plain rc=$?"
-EXTRA=""
-[ "$TOOL" = racecheck ] && EXTRA="--racecheck-report all"
-timeout 2400 /usr/local/cuda/bin/compute-sanitizer --tool $TOOL $EXTRA --error-exitcode 9 \
-  python tools/sanitize_run.py $N > gpurun_out/r2/sanitizer/$TOOL.log 2>&1
-echo "$TOOL rc=$?"; tail -5 gpurun_out/r2/sanitizer/$TOOL.log
+timeout 1200 python tools/sanitize_run.py $N > gpurun_out/r2/sanitizer/product.log 2>&1
+echo "product rc=$?"; tail -2 gpurun_out/r2/sanitizer/product.log
+timeout 1800 python tools/sanitize_run.py $N --checked > gpurun_out/r2/sanitizer/checked.log 2>&1
+echo "checked rc=$?"; tail -3 gpurun_out/r2/sanitizer/checked.log

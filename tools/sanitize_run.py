@@ -8,6 +8,13 @@ generic-bins context.  Results are checked against the oracle so a run that
 the sanitizer perturbs still has to be correct.
 
 usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py [c2_frames]
+       python tools/sanitize_run.py [c2_frames] --checked
+The pool's compute-sanitizer is closed ("runs under it have left GPUs needing
+a reset"), so --checked runs the same workload on the bounds-checked build of
+the library (-DCLIPDETECT_CHECKED: every TMA source range, ring hand-off,
+shared-memory code offset, code -> bin entry, K3 alive / run / chunk index and
+K4 staged row is checked on the device; a failure prints the condition and
+traps, which fails the call).
 """
 import os
 import sys
@@ -22,11 +29,21 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 from synth import manifest  # noqa: E402
 from paper_2503_12964_b200 import Ctx, default_params  # noqa: E402
+from paper_2503_12964_b200 import _build, clipdetect  # noqa: E402
 from paper_2503_12964_b200.clipdetect import FORMAT_NV12  # noqa: E402
 
 
 def main():
-    n_c2 = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    n_c2 = int(args[0]) if args else 200
+    if "--checked" in sys.argv:
+        import glob
+        import re
+        lib = _build.build(checked=True)
+        clipdetect.load(path=lib)
+        sites = sum(len(re.findall(r"\bCD_CHECK\(", open(f).read()))
+                    for f in glob.glob(os.path.join(ROOT, "paper_2503_12964_b200", "csrc", "*.cu")))
+        print(f"checked build {lib}: {sites} CD_CHECK sites compiled in")
     dev = torch.device("cuda:0")
     ctx = Ctx(device=0)
     vids = [manifest.c1_video(), manifest.subsample(manifest.c2_video(0), n_c2)]
