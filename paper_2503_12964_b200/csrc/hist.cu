@@ -52,24 +52,15 @@ constexpr int kLutBytes = 65536;
 // runtime addressing if it ever differs (k1_consume<MODE, false>).
 constexpr uint32_t kDynSmemBase = 0x400;
 
-// What the consumers need to know about the stage in a ring slot, written by
-// the producer before it arms the slot's "full" barrier (whose completion
-// orders it for the consumers): the consumers run no iterator of their own.
-struct StageMeta {
-  uint32_t* gh;   // the frame's global histogram, when this stage is its last; else null
-  int32_t ng;     // 48-byte groups in the stage
-  int32_t seq;    // the stage's index in the CTA's range (checked builds verify the hand-off)
-};
-
 struct K1Smem {
   alignas(128) uint8_t buf[kStages][kStageGroups * 48];
-  StageMeta meta[kStages];
   uint8_t lut[kLutBytes];   // hue table: lut[lut_index(na, d)] = lut_entry_dir(na, d, kHashRgb)
   uint32_t hist[kDirCodes];  // CTA-shared code histogram (bins for kModeGeneric)
   uint8_t c2b[kDirCodes];    // code -> bin
   uint64_t full[kStages];
   uint64_t empty[kStages];
   MadK mk;
+  int32_t seq[kStages];  // checked builds: the stage index the producer put in each slot
 };
 constexpr uint32_t kLutOff = (uint32_t)offsetof(K1Smem, lut);
 constexpr uint32_t kHistOff = (uint32_t)offsetof(K1Smem, hist);
@@ -82,10 +73,8 @@ struct StageIter {
   int32_t stages, last_ng, n_frames;
   int64_t groups;
   const uint8_t* frames;
-  uint32_t* hist;
   __device__ void load() {
     const HistSeg& g = segs[seg];
-    hist = g.hist;
     groups = g.groups;
     stages = (int32_t)g.stages;
     n_frames = (int32_t)g.n_frames;
@@ -200,9 +189,10 @@ __device__ __forceinline__ void bin_group_generic(const uint8_t* src, uint32_t* 
 
 // The consumer loop (IMM: see lut_ld).
 template <int MODE, bool IMM>
-__device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, int32_t n, uint32_t nh,
+__device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const HistSeg* segs,
+                                           int32_t nseg, int64_t s_begin, int32_t n, uint32_t nh,
                                            uint32_t ns, uint32_t nv, uint32_t* sink) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t nbins = nh * ns * nv;
   // multiplier constants through shared memory: opaque registers for ptxas
   MadK mk;
@@ -213,12 +203,13 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, int32_t n
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t xacc = 0;
+  StageIter it;
+  it.seek(segs, nseg, s_begin);
   uint32_t slot = 0, par = 0;
   for (int32_t i = 0; i < n; ++i) {
+    const int ng = it.ng();
     mbar_wait(&sm.full[slot], par);
-    const StageMeta meta = sm.meta[slot];
-    const int ng = meta.ng;
-    CD_CHECK(meta.seq == i && ng >= 1 && ng <= kStageGroups);  // the slot holds stage i
+    CD_CHECK(sm.seq[slot] == i && ng >= 1 && ng <= kStageGroups);  // the slot holds stage i
     const uint8_t* buf = sm.buf[slot];
     if constexpr (MODE == kModeFast) {
       if (ng == kStageGroups) {
@@ -236,20 +227,27 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, int32_t n
         xacc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w;
       }
     }
-    mbar_arrive(&sm.empty[slot]);  // every consumer lane: its reads of the slot are done
-    slot = slot == kStages - 1 ? 0u : slot + 1;
-    par ^= slot == 0 ? 1u : 0u;
-    if (MODE != kModeRead && meta.gh != nullptr) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    if (++slot == kStages) {
+      slot = 0;
+      par ^= 1u;
+    }
+    const int32_t seg_now = it.seg, frame_now = it.frame;
+    const bool last = (i + 1 == n);
+    const bool changed = it.next(!last);
+    if (MODE != kModeRead && (last || changed)) {
       // flush the frame's partial code histogram straight to the frame's global
       // bins: one RED per non-zero code, two named barriers among the consumers
       named_bar_sync(1, kConsumers);
+      uint32_t* gh = segs[seg_now].hist + (int64_t)frame_now * nbins;
       const uint32_t nentries = MODE == kModeFast ? (uint32_t)kDirCodes : nbins;
       for (uint32_t c = tid; c < nentries; c += kConsumers) {
         const uint32_t cnt = sm.hist[c];
         if (cnt) {
           sm.hist[c] = 0u;
           CD_CHECK((MODE == kModeFast ? sm.c2b[c] : c) < nbins);  // only reachable codes counted
-          atomicAdd(meta.gh + (MODE == kModeFast ? sm.c2b[c] : c), cnt);
+          atomicAdd(gh + (MODE == kModeFast ? sm.c2b[c] : c), cnt);
         }
       }
       named_bar_sync(1, kConsumers);
@@ -283,7 +281,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kConsumers);
+      mbar_init(&sm.empty[i], kWarps);
     }
     fence_mbar_init();
   }
@@ -298,20 +296,17 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       StageIter it;
       it.seek(segs, nseg, s_begin);
       uint32_t slot = 0, par = 0;
-      const uint32_t nbins = nh * ns * nv;
       for (int32_t i = 0; i < n; ++i) {
         if (i >= kStages) mbar_wait(&sm.empty[slot], par ^ 1u);
-        const int32_t ng = it.ng();
-        const uint8_t* src = it.src();
-        const uint32_t bytes = (uint32_t)ng * 48u;
-        CD_CHECK(ng >= 1 && ng <= kStageGroups && (reinterpret_cast<uintptr_t>(src) & 15) == 0);
-        CD_CHECK(src >= it.frames && src + bytes <= it.frames + (int64_t)it.n_frames * it.groups * 48);
-        uint32_t* gh = it.hist + (int64_t)it.frame * nbins;
-        const bool last = i + 1 == n;
-        const bool changed = it.next(!last);  // the frame ends with this stage
-        sm.meta[slot] = StageMeta{(last || changed) ? gh : nullptr, ng, i};
-        mbar_arrive_expect_tx(&sm.full[slot], bytes);  // release: orders the meta store
-        bulk_g2s(sm.buf[slot], src, bytes, &sm.full[slot], pol);
+        const uint32_t bytes = (uint32_t)it.ng() * 48u;
+        CD_CHECK(bytes >= 48 && bytes <= kStageGroups * 48 && (reinterpret_cast<uintptr_t>(it.src()) & 15) == 0);
+        CD_CHECK(it.src() >= it.frames && it.src() + bytes <= it.frames + (int64_t)it.n_frames * it.groups * 48);
+#ifdef CLIPDETECT_CHECKED
+        sm.seq[slot] = i;  // ordered before the consumers' wait by the arrive's release
+#endif
+        mbar_arrive_expect_tx(&sm.full[slot], bytes);
+        bulk_g2s(sm.buf[slot], it.src(), bytes, &sm.full[slot], pol);
+        it.next(i + 1 < n);
         if (++slot == kStages) {
           slot = 0;
           par ^= 1u;
@@ -323,9 +318,9 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   // ------------------------------------------------------------ consumers
   const uint32_t sbase = smem_u32(smem_raw);
   if (sbase == kDynSmemBase)
-    k1_consume<MODE, true>(sm, sbase, n, nh, ns, nv, sink);
+    k1_consume<MODE, true>(sm, sbase, segs, nseg, s_begin, n, nh, ns, nv, sink);
   else
-    k1_consume<MODE, false>(sm, sbase, n, nh, ns, nv, sink);
+    k1_consume<MODE, false>(sm, sbase, segs, nseg, s_begin, n, nh, ns, nv, sink);
 }
 
 }  // namespace

@@ -244,7 +244,8 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
         ++br;
       }
     }
-    mbar_arrive(&sm.empty[slot]);  // every consumer lane: its reads of the slot are done
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[slot]);
     if (++slot == kNvStages) {
       slot = 0;
       par ^= 1u;
@@ -309,7 +310,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kNvStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kNvConsumers);
+      mbar_init(&sm.empty[i], kNvWarps);
     }
     fence_mbar_init();
   }

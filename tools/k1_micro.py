@@ -30,7 +30,12 @@ def timeit(fn, stream, reps=5):
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 6000
+    args = [a for a in sys.argv[1:] if not a.startswith("--lib=")]
+    libs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--lib=")]
+    if libs:  # A/B of another build of the library (tools only)
+        from paper_2503_12964_b200 import clipdetect
+        clipdetect.load(path=os.path.abspath(libs[0]))
+    n = int(args[0]) if args else 6000
     dev = torch.device("cuda:0")
     synth.build(device=True)
     stream = torch.cuda.Stream()
@@ -57,6 +62,7 @@ def main():
                      "hist_sha16": hashlib.sha256(hist.cpu().numpy().tobytes()).hexdigest()[:16]}
         del frames, hist
         torch.cuda.empty_cache()
+    out["lib"] = libs[0] if libs else "product"
     print(json.dumps(out))
 
 
