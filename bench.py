@@ -278,13 +278,16 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     st = ctx.stats(reset=True)
     per_rank_ms = [ms / args.steps]
+    per_rank_k1 = [st["k1_ms"] / args.steps]
     gather_ms = 1000.0 * gather_wall[0] / max(1, args.steps + args.warmup)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        allt = torch.empty(world, dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, st["k1_ms"]], dtype=torch.float64, device=dev)
+        allt = torch.empty(2 * world, dtype=torch.float64, device=dev)
         dist.all_gather_into_tensor(allt, t)
-        per_rank_ms = [x / args.steps for x in allt.cpu().tolist()]
-        ms_max = max(allt.cpu().tolist())
+        allt = allt.view(world, 2).cpu().tolist()
+        per_rank_ms = [x[0] / args.steps for x in allt]
+        per_rank_k1 = [x[1] / args.steps for x in allt]
+        ms_max = max(x[0] for x in allt)
     else:
         ms_max = ms
     ms_step = ms_max / args.steps
@@ -477,6 +480,7 @@ def run_ours(args):
                                "k3": round(st["k3_ms"] / args.steps, 4)},
         "gpu_launches": int(st["launches"]),
         "per_rank_ms_per_step": [round(x, 4) for x in per_rank_ms],
+        "per_rank_k1_ms_per_step": [round(x, 4) for x in per_rank_k1],
         "gather_wall_ms_per_step_rank0": round(gather_ms, 4) if world > 1 else None,
         "clocks": clk_sum,
         "parity_vs_golden": parity,

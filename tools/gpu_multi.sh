@@ -11,3 +11,5 @@ timeout 900 python bench.py --gpus $N --shard-frames --steps 10 --warmup 3 > gpu
 echo "shard n=$N rc=$?"; tail -c 400 gpurun_out/r2/multi/shard_n$N.log
 timeout 1200 python bench.py --gpus $N --config C5 --steps 2 --warmup 1 > gpurun_out/r2/multi/c5_n$N.log 2> gpurun_out/r2/multi/c5_n$N.err
 echo "c5 n=$N rc=$?"; tail -c 400 gpurun_out/r2/multi/c5_n$N.log
+timeout 600 python bench.py --gpus $N --steps 10 --warmup 3 --no-cpu --no-gather --no-c3 --no-noise --no-e2e --sample-k 0 > gpurun_out/r2/multi/nogather_n$N.log 2> gpurun_out/r2/multi/nogather_n$N.err
+echo "nogather n=$N rc=$?"; tail -c 300 gpurun_out/r2/multi/nogather_n$N.log
