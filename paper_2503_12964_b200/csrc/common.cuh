@@ -80,6 +80,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// The same wait with a back-off, for the producer lanes: spinning there steals
+// issue slots from the consumer warps of its scheduler, which then release ring
+// slots last for the whole CTA (B200 A/B with the L2 prefetch below: K1 +2.5 %,
+// profiles/r02/ab/).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  while (!done) {
+    __nanosleep(256);
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
 // bytes and both addresses must be multiples of 16.  L2 evict-first: frame
 // bytes are read exactly once.
@@ -90,6 +105,12 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
       " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+// L2 prefetch of a global range (TMA bulk prefetch; no shared memory, no
+// barrier): lets a producer run further ahead than its ring is deep.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -326,7 +326,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       it.seek(segs, nseg, s_begin);
       uint32_t slot = 0, par = 0;
       for (int32_t i = 0; i < n; ++i) {
-        if (i >= kNvStages) mbar_wait(&sm.empty[slot], par ^ 1u);
+        if (i >= kNvStages) mbar_wait_sleep(&sm.empty[slot], par ^ 1u);
         const int32_t nr = it.nr(), W = it.W;
         const uint32_t ybytes = 2u * nr * W, cbytes = (uint32_t)nr * W;
         const uint8_t* ysrc = it.frame_base() + 2 * (int64_t)it.st * it.R * W;
