@@ -303,17 +303,23 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       StageIter pf;
       pf.seek(segs, nseg, s_begin);
       int32_t pf_i = 0;
-      for (; pf_i < kPf && pf_i < n; ++pf_i) {
+      // (the read-only probe K6 measures the plain ring: no prefetch, no sleep)
+      for (; MODE != kModeRead && pf_i < kPf && pf_i < n; ++pf_i) {
         if (pf_i >= kStages) bulk_prefetch_l2(pf.src(), (uint32_t)pf.ng() * 48u);
         pf.next(pf_i + 1 < n);
       }
       uint32_t slot = 0, par = 0;
       for (int32_t i = 0; i < n; ++i) {
-        if (pf_i < n) {
+        if (MODE != kModeRead && pf_i < n) {
           bulk_prefetch_l2(pf.src(), (uint32_t)pf.ng() * 48u);
           pf.next(++pf_i < n);
         }
-        if (i >= kStages) mbar_wait_sleep(&sm.empty[slot], par ^ 1u);
+        if (i >= kStages) {
+          if (MODE == kModeRead)
+            mbar_wait(&sm.empty[slot], par ^ 1u);
+          else
+            mbar_wait_sleep(&sm.empty[slot], par ^ 1u);
+        }
         const uint32_t bytes = (uint32_t)it.ng() * 48u;
         CD_CHECK(bytes >= 48 && bytes <= kStageGroups * 48 && (reinterpret_cast<uintptr_t>(it.src()) & 15) == 0);
         CD_CHECK(it.src() >= it.frames && it.src() + bytes <= it.frames + (int64_t)it.n_frames * it.groups * 48);

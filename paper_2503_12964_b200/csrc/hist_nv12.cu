@@ -244,8 +244,9 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
         ++br;
       }
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[slot]);
+    // every consumer lane releases the slot (its reads are done; no warp sync:
+    // B200 A/B +1.4 % over one release per warp, the reverse of K1)
+    mbar_arrive(&sm.empty[slot]);
     if (++slot == kNvStages) {
       slot = 0;
       par ^= 1u;
@@ -310,7 +311,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kNvStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kNvWarps);
+      mbar_init(&sm.empty[i], kNvConsumers);
     }
     fence_mbar_init();
   }
@@ -326,7 +327,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       it.seek(segs, nseg, s_begin);
       uint32_t slot = 0, par = 0;
       for (int32_t i = 0; i < n; ++i) {
-        if (i >= kNvStages) mbar_wait_sleep(&sm.empty[slot], par ^ 1u);
+        if (i >= kNvStages) mbar_wait(&sm.empty[slot], par ^ 1u);
         const int32_t nr = it.nr(), W = it.W;
         const uint32_t ybytes = 2u * nr * W, cbytes = (uint32_t)nr * W;
         const uint8_t* ysrc = it.frame_base() + 2 * (int64_t)it.st * it.R * W;

@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for r in $(seq 1 $R); do
   for lib in "$@"; do
     if [ "$lib" = product ]; then a=""; else a="--lib=$lib"; fi
-    timeout 300 python tools/k1_micro.py 6000 $a >> gpurun_out/r2/ab/k1.jsonl 2>> gpurun_out/r2/ab/err.log
+    timeout 300 python tools/k1_micro.py ${K1N:-6000} $a >> gpurun_out/r2/ab/k1.jsonl 2>> gpurun_out/r2/ab/err.log
     timeout 300 python tools/nv12_micro.py 6000 $a >> gpurun_out/r2/ab/nv12.jsonl 2>> gpurun_out/r2/ab/err.log
   done
 done
