@@ -11,7 +11,7 @@
 //    frame) HBM -> shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
 //    mbarrier::complete_tx, L2 evict_first) into a 3-deep mbarrier ring, with
 //    TMA L2 prefetches three stages further ahead, and sleeps while it waits;
-//    consumer warps release a slot per warp ("empty" barrier);
+//    every consumer lane releases the slot it has read ("empty" barrier);
 //  * 20 consumer warps; each lane takes 5 lane-contiguous 4-pixel quads of a
 //    stage (three conflict-free LDS.32 each, so one warp instruction covers
 //    128 adjacent pixels), unpacks them into u16x2 pixel pairs and computes a
@@ -228,8 +228,7 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const His
         xacc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    mbar_arrive(&sm.empty[slot]);  // every consumer lane: its reads of the slot are done
     if (++slot == kStages) {
       slot = 0;
       par ^= 1u;
@@ -282,7 +281,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
     sm.mk = mk_param;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], kWarps);
+      mbar_init(&sm.empty[i], kConsumers);
     }
     fence_mbar_init();
   }
