@@ -193,7 +193,7 @@ template <int MODE, bool IMM>
 __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const HistSeg* segs,
                                            int32_t nseg, int64_t s_begin, int32_t n, uint32_t nh,
                                            uint32_t ns, uint32_t nv, uint32_t* sink) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const uint32_t nbins = nh * ns * nv;
   // multiplier constants through shared memory: opaque registers for ptxas
   MadK mk;
