@@ -298,22 +298,21 @@ bool is_device_ptr(const void* p) {
 }
 
 // ------------------------------------------------------------------ merge core
-// Runs K3 on the detected cuts (device, per video at cut_base) of nv videos.
-// Writes final cuts (same layout), n_final[v] (device) and detected cosines.
-struct MergeOut {
-  int64_t band_hits_total = 0;
-  std::vector<int64_t> vstate;  // [nv][4]
-};
-
+// Enqueues K3 on the detected cuts (device, per video at cut_base) of nv
+// videos; nothing is read back here.  mvh: emb, n, cut_base per video, and
+// n_clips when d_ncuts is null (else the device fills n_clips / clip_base from
+// K2's counts).  Kub >= the clip count K (the host knows only this bound when
+// the counts stay on the device).  Writes final cuts (same layout), n_final[v]
+// and detected cosines (device); the per-video state [nv][4] is in ctx->m_vstate.
 int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, const int32_t* d_cuts,
-              int32_t* d_final, int32_t* d_nfinal, double* d_detcos, MergeOut& mo) {
+              const int32_t* d_ncuts, int64_t Kub, int32_t* d_final, int32_t* d_nfinal,
+              double* d_detcos) {
   const int32_t nv = (int32_t)mvh.size();
-  int64_t K = 0, pieces = 0;
-  for (auto& m : mvh) {
-    K += m.n_clips;
-    pieces += (m.n + kPieceFrames - 1) / kPieceFrames;
-  }
-  pieces += K;
+  int64_t pieces = Kub;  // sum over clips of ceil(len / kPieceFrames) <= n / kPieceFrames + clips
+  for (auto& m : mvh) pieces += (m.n + kPieceFrames - 1) / kPieceFrames;
+  if (Kub > INT32_MAX || pieces > INT32_MAX)
+    return fail(ctx, CLIP_E_INVALID, "too many clips for one merge (%lld)", (long long)Kub);
+  const int64_t K = Kub;
   CKS(ensure(ctx, ctx->m_video, sizeof(MergeVideo) * nv));
   CKS(ensure(ctx, ctx->m_clip_video, 4 * K));
   CKS(ensure(ctx, ctx->m_f0, 4 * K));
@@ -327,10 +326,9 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   CKS(ensure(ctx, ctx->m_cos_clip, 8 * K));
   CKS(ensure(ctx, ctx->m_norm2, 8 * K));
   CKS(ensure(ctx, ctx->m_runs, 4 * (4 * K + 1)));
-  CKS(ensure(ctx, ctx->m_counters, 8 * 8));
+  CKS(ensure(ctx, ctx->m_counters, 8 * 9));
   CKS(ensure(ctx, ctx->m_vstate, 8 * 4 * nv));
   CKS(ensure(ctx, ctx->m_valive, 8 * nv));
-  CKS(ensure_pinned(ctx, std::max<size_t>(64, 8 * 4 * (size_t)nv)));
   CK(cudaMemcpyAsync(ctx->m_video.p, mvh.data(), sizeof(MergeVideo) * nv, cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaMemsetAsync(ctx->m_cos_clip.p, 0, 8 * K, ctx->stream));
@@ -351,38 +349,83 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   s.run_hi = s.run_lo + K;
   s.run_cbase = s.run_hi + K;
   s.counters = P<int64_t>(ctx->m_counters);
+  s.Kd = reinterpret_cast<int32_t*>(s.counters + 8);
   s.vstate = P<int64_t>(ctx->m_vstate);
   s.valive = P<int64_t>(ctx->m_valive);
-  const MergeVideo* d_mv = P<MergeVideo>(ctx->m_video);
+  MergeVideo* d_mv = P<MergeVideo>(ctx->m_video);
 
   Span sp(ctx, 2);
-  CK(k3_prepare_launch(d_mv, nv, (int32_t)K, d_cuts, s, ctx->stream));
-  CK(k3_piece_sum_launch(d_mv, nv, (int32_t)K, dim, pieces,
-                         ctx->p.emb_stride > 1 ? (int32_t)ctx->p.emb_stride : 1, s, ctx->stream));
+  CK(k3_prepare_launch(d_mv, nv, (int32_t)K, d_ncuts, d_cuts, s, ctx->stream));
+  CK(k3_piece_sum_launch(d_mv, dim, pieces, ctx->p.emb_stride > 1 ? (int32_t)ctx->p.emb_stride : 1,
+                         s, ctx->stream));
   CK(k3_clip_sum_launch((int32_t)K, dim, s, ctx->stream));
-  ctx->stats.launches += 4;
+  ctx->stats.launches += 5;
   if (K - nv > 0) {
-    CK(k3_rounds_launch(d_mv, nv, (int32_t)K, dim, K - nv, ctx->p.merge_cos_threshold, ctx->p.band_rel,
+    CK(k3_rounds_launch(d_mv, nv, dim, K - nv, ctx->p.merge_cos_threshold, ctx->p.band_rel,
                         (int32_t)ctx->p.max_merge_rounds, ctx->sm_count, s, ctx->stream));
     ctx->stats.launches += 1;
   }
   CK(k3_finish_launch(d_mv, nv, (int32_t)K, s, d_final, d_nfinal, d_detcos, ctx->stream));
   ctx->stats.launches += 1;
   sp.end();
-  CK(cudaMemcpyAsync(ctx->hpin, s.vstate, 8 * 4 * nv, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  ctx->stats.memcpy_d2h += 8 * 4 * nv;
-  mo.vstate.assign(reinterpret_cast<int64_t*>(ctx->hpin), reinterpret_cast<int64_t*>(ctx->hpin) + 4 * nv);
   return CLIP_OK;
 }
 
-// pack per-video detected / final cuts and cosines into contiguous buffers
+// Result summary of a clip_run_videos call, one int64 row per video (after a
+// leading total): the counts and state the host reports, and the video's
+// offset in the packed cut buffer (exclusive scan of 2 * n_detected).
+enum { SUM_NCUTS = 0, SUM_NCAND, SUM_NFINAL, SUM_OFF, SUM_BAND, SUM_ROUNDS, SUM_W };
+
+__global__ void __launch_bounds__(1024)
+summary_kernel(int32_t nvid, const int32_t* __restrict__ ncuts, const int32_t* __restrict__ ncand,
+               const int32_t* __restrict__ nfin, const int64_t* __restrict__ vstate,
+               int64_t* __restrict__ sum) {
+  __shared__ int64_t wsum[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t carry = 0;
+  for (int32_t base = 0; base < nvid; base += 1024) {
+    const int32_t v = base + threadIdx.x;
+    const int64_t x = v < nvid ? 2 * (int64_t)ncuts[v] : 0;
+    int64_t inc = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t w = wsum[lane];
+      int64_t wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      wsum[lane] = wi - w;
+      if (lane == 31) wsum[32] = wi;
+    }
+    __syncthreads();
+    if (v < nvid) {
+      int64_t* r = sum + 1 + (int64_t)SUM_W * v;
+      r[SUM_NCUTS] = ncuts[v];
+      r[SUM_NCAND] = ncand[v];
+      r[SUM_NFINAL] = nfin ? nfin[v] : ncuts[v];
+      r[SUM_OFF] = carry + wsum[warp] + inc - x;
+      r[SUM_BAND] = vstate ? vstate[4 * v + 2] : 0;
+      r[SUM_ROUNDS] = vstate ? vstate[4 * v + 1] : 0;
+    }
+    carry += wsum[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sum[0] = carry;
+}
+
+// pack per-video detected / final cuts and cosines into contiguous buffers:
+// video v at sum row v's offset, [detected | final (n_detected reserved)]
 __global__ void pack_kernel(const VideoDesc* __restrict__ vids, int32_t nvid, int64_t F,
                             const int32_t* __restrict__ cuts, const int32_t* __restrict__ ncuts,
                             const int32_t* __restrict__ fin, const int32_t* __restrict__ nfin,
-                            const double* __restrict__ detcos, const int64_t* __restrict__ det_off,
-                            const int64_t* __restrict__ fin_off, int32_t* __restrict__ out,
-                            double* __restrict__ out_cos) {
+                            const double* __restrict__ detcos, const int64_t* __restrict__ sum,
+                            int32_t* __restrict__ out, double* __restrict__ out_cos) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= F) return;
   int32_t lo = 0, hi = nvid - 1;
@@ -391,11 +434,12 @@ __global__ void pack_kernel(const VideoDesc* __restrict__ vids, int32_t nvid, in
     if (vids[m].fbase <= i) lo = m; else hi = m - 1;
   }
   const int64_t j = i - vids[lo].fbase;
+  const int64_t det_off = sum[1 + (int64_t)SUM_W * lo + SUM_OFF];
   if (j < ncuts[lo]) {
-    out[det_off[lo] + j] = cuts[i];
-    if (out_cos) out_cos[det_off[lo] + j] = detcos ? detcos[i] : 0.0;
+    out[det_off + j] = cuts[i];
+    if (out_cos) out_cos[det_off + j] = detcos ? detcos[i] : 0.0;
   }
-  if (fin && j < nfin[lo]) out[fin_off[lo] + j] = fin[i];
+  if (j < nfin[lo]) out[det_off + ncuts[lo] + j] = fin[i];
 }
 
 }  // namespace
@@ -617,16 +661,21 @@ int clip_merge(clip_ctx* ctx, const float* emb, int64_t n_frames, int32_t dim,
   mv[0].clip_base = 0;
   mv[0].n_clips = (int32_t)n_cuts + 1;
   CKS(ensure(ctx, ctx->nfinal, 4));
-  MergeOut mo;
-  CKS(run_merge(ctx, mv, dim, cuts, merged, P<int32_t>(ctx->nfinal), boundary_cos, mo));
-  int32_t nf = 0;
-  CK(cudaMemcpyAsync(ctx->hpin, ctx->nfinal.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CKS(ensure_pinned(ctx, 64));
+  CKS(run_merge(ctx, mv, dim, cuts, nullptr, n_cuts + 1, merged, P<int32_t>(ctx->nfinal),
+                boundary_cos));
+  // one read-back: the video state [4] and n_final
+  int64_t* hp = reinterpret_cast<int64_t*>(ctx->hpin);
+  CK(cudaMemcpyAsync(hp, ctx->m_vstate.p, 8 * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hp + 4, ctx->nfinal.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  memcpy(&nf, ctx->hpin, 4);
+  ctx->stats.memcpy_d2h += 8 * 4 + 4;
+  int32_t nf = 0;
+  memcpy(&nf, hp + 4, 4);
   harvest(ctx);
   *n_merged = nf;
-  if (n_band_hits) *n_band_hits = mo.vstate[2];
-  if (rounds) *rounds = (int32_t)mo.vstate[1];
+  if (n_band_hits) *n_band_hits = hp[2];
+  if (rounds) *rounds = (int32_t)hp[1];
   return CLIP_OK;
 }
 
@@ -684,7 +733,6 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
   CKS(ensure(ctx, ctx->final_cuts, 4 * F));
   CKS(ensure(ctx, ctx->nfinal, 4 * n_videos));
   CKS(ensure(ctx, ctx->detcos, 8 * F));
-  CKS(ensure_pinned(ctx, 16 * (size_t)n_videos + 64));
 
   Span whole(ctx, 3);
   CK(cudaMemcpyAsync(ctx->vids.p, vd.data(), sizeof(VideoDesc) * n_videos, cudaMemcpyHostToDevice,
@@ -818,80 +866,75 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
     sp.end();
     ctx->stats.launches += 2;
   }
-  // counts -> host (sync #1)
-  CK(cudaMemcpyAsync(ctx->hpin, ctx->ncuts.p, 4 * n_videos, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(reinterpret_cast<int32_t*>(ctx->hpin) + n_videos, ctx->ncand.p, 4 * n_videos,
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  ctx->stats.memcpy_d2h += 8 * n_videos;
-  std::vector<int32_t> ncuts(reinterpret_cast<int32_t*>(ctx->hpin),
-                             reinterpret_cast<int32_t*>(ctx->hpin) + n_videos);
-  std::vector<int32_t> ncand(reinterpret_cast<int32_t*>(ctx->hpin) + n_videos,
-                             reinterpret_cast<int32_t*>(ctx->hpin) + 2 * n_videos);
-
-  // ---- K3: merge
-  MergeOut mo;
-  mo.vstate.assign(4 * n_videos, 0);
+  // ---- K3: merge (the cut counts stay on the device: K3 sizes itself from
+  // them, the host passes the min-clip-length bound)
   int32_t* d_final = P<int32_t>(ctx->final_cuts);
   if (merge) {
     std::vector<MergeVideo> mv(n_videos);
-    int32_t cb = 0;
+    int64_t Kub = 0;
     for (int32_t i = 0; i < n_videos; ++i) {
       mv[i].emb = videos[i].emb;
       mv[i].n = videos[i].n_frames;
       mv[i].cut_base = vd[i].fbase;
-      mv[i].clip_base = cb;
-      mv[i].n_clips = ncuts[i] + 1;
-      cb += ncuts[i] + 1;
+      mv[i].clip_base = 0;
+      mv[i].n_clips = 0;
+      Kub += videos[i].n_frames / L + 1;
     }
-    CKS(run_merge(ctx, mv, dim, P<int32_t>(ctx->cuts), d_final, P<int32_t>(ctx->nfinal),
-                  P<double>(ctx->detcos), mo));
+    CKS(run_merge(ctx, mv, dim, P<int32_t>(ctx->cuts), P<int32_t>(ctx->ncuts), Kub, d_final,
+                  P<int32_t>(ctx->nfinal), P<double>(ctx->detcos)));
   }
 
-  // ---- pack results: per video [detected | final (n_detected reserved)]
-  std::vector<int64_t> offs(2 * n_videos);
-  int64_t total = 0;
-  for (int32_t i = 0; i < n_videos; ++i) {
-    offs[i] = total;
-    offs[n_videos + i] = total + ncuts[i];
-    total += 2 * (int64_t)ncuts[i];
-  }
-  CKS(ensure(ctx, ctx->pack, 4 * std::max<int64_t>(1, total) + 16 * n_videos + 16));
-  CKS(ensure(ctx, ctx->pack_cos, 8 * std::max<int64_t>(1, total)));
-  int64_t* d_offs = reinterpret_cast<int64_t*>(P<uint8_t>(ctx->pack) + 4 * std::max<int64_t>(1, total));
-  // offsets go after the packed cuts (8-byte aligned: total*4 rounded)
-  d_offs = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(d_offs) + 7) & ~(uintptr_t)7);
-  CK(cudaMemcpyAsync(d_offs, offs.data(), 16 * n_videos, cudaMemcpyHostToDevice, ctx->stream));
+  // ---- pack results: per video [detected | final (n_detected reserved)] at
+  // offsets scanned on the device; ONE read-back of summary + packed cuts
+  // (sized by the capacity bound `need` >= the packed total) and one sync.
+  const int64_t sum_words = 1 + (int64_t)SUM_W * n_videos;
+  CKS(ensure(ctx, ctx->pack, 8 * sum_words + 4 * need));
   const bool want_cos = merge && out && out->detected_cos;
+  if (want_cos) CKS(ensure(ctx, ctx->pack_cos, 8 * need));
+  const size_t pin_cos = (size_t)(8 * sum_words + 4 * need + 7) & ~(size_t)7;
+  CKS(ensure_pinned(ctx, pin_cos + (want_cos ? 8 * need : 0)));
+  int64_t* d_sum = P<int64_t>(ctx->pack);
+  int32_t* d_pack = reinterpret_cast<int32_t*>(d_sum + sum_words);
+  summary_kernel<<<1, 1024, 0, ctx->stream>>>(n_videos, P<int32_t>(ctx->ncuts), P<int32_t>(ctx->ncand),
+                                              merge ? P<int32_t>(ctx->nfinal) : nullptr,
+                                              merge ? P<int64_t>(ctx->m_vstate) : nullptr, d_sum);
+  CK(cudaGetLastError());
   pack_kernel<<<(unsigned)((F + 255) / 256), 256, 0, ctx->stream>>>(
       P<VideoDesc>(ctx->vids), n_videos, F, P<int32_t>(ctx->cuts), P<int32_t>(ctx->ncuts),
       merge ? d_final : P<int32_t>(ctx->cuts), merge ? P<int32_t>(ctx->nfinal) : P<int32_t>(ctx->ncuts),
-      want_cos ? P<double>(ctx->detcos) : nullptr, d_offs, d_offs + n_videos, P<int32_t>(ctx->pack),
+      want_cos ? P<double>(ctx->detcos) : nullptr, d_sum, d_pack,
       want_cos ? P<double>(ctx->pack_cos) : nullptr);
   CK(cudaGetLastError());
-  ctx->stats.launches += 1;
-  if (merge) {
-    CK(cudaMemcpyAsync(ctx->hpin, ctx->nfinal.p, 4 * n_videos, cudaMemcpyDeviceToHost, ctx->stream));
-  }
-  if (total > 0)
-    CK(cudaMemcpyAsync(cut_buf, ctx->pack.p, 4 * total, cudaMemcpyDeviceToHost, ctx->stream));
-  if (want_cos && total > 0)
-    CK(cudaMemcpyAsync(out->detected_cos, ctx->pack_cos.p, 8 * total, cudaMemcpyDeviceToHost,
-                       ctx->stream));
+  ctx->stats.launches += 2;
+  CK(cudaMemcpyAsync(ctx->hpin, ctx->pack.p, 8 * sum_words + 4 * need, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if (want_cos)
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->hpin) + pin_cos, ctx->pack_cos.p, 8 * need,
+                       cudaMemcpyDeviceToHost, ctx->stream));
   whole.end();
   CK(cudaStreamSynchronize(ctx->stream));
-  ctx->stats.memcpy_d2h += 4 * total + (merge ? 4 * n_videos : 0) + (want_cos ? 8 * total : 0);
+  ctx->stats.memcpy_d2h += 8 * sum_words + 4 * need + (want_cos ? 8 * need : 0);
+  const int64_t* hs = static_cast<const int64_t*>(ctx->hpin);
+  const int64_t total = hs[0];
+  if (total > need)  // K2 keeps every clip >= min_clip_frames: cannot happen
+    return fail(ctx, CLIP_E_CUDA, "packed cuts %lld exceed the bound %lld", (long long)total,
+                (long long)need);
+  if (total > 0) {
+    memcpy(cut_buf, hs + sum_words, 4 * total);
+    if (want_cos) memcpy(out->detected_cos, static_cast<uint8_t*>(ctx->hpin) + pin_cos, 8 * total);
+  }
   for (int32_t i = 0; i < n_videos; ++i) {
-    clip_video_result& r = results[i];
-    memset(&r, 0, sizeof r);
-    r.id = videos[i].id;
-    r.n_candidates = ncand[i];
-    r.n_detected = ncuts[i];
-    r.n_final = merge ? reinterpret_cast<int32_t*>(ctx->hpin)[i] : ncuts[i];
-    r.n_band_hits = mo.vstate[4 * i + 2];
-    r.rounds = (int32_t)mo.vstate[4 * i + 1];
-    r.detected_offset = offs[i];
-    r.final_offset = offs[n_videos + i];
+    const int64_t* r = hs + 1 + (int64_t)SUM_W * i;
+    clip_video_result& res = results[i];
+    memset(&res, 0, sizeof res);
+    res.id = videos[i].id;
+    res.n_candidates = (int32_t)r[SUM_NCAND];
+    res.n_detected = (int32_t)r[SUM_NCUTS];
+    res.n_final = (int32_t)r[SUM_NFINAL];
+    res.n_band_hits = r[SUM_BAND];
+    res.rounds = (int32_t)r[SUM_ROUNDS];
+    res.detected_offset = r[SUM_OFF];
+    res.final_offset = r[SUM_OFF] + r[SUM_NCUTS];
   }
   harvest(ctx);
   return CLIP_OK;

@@ -100,26 +100,31 @@ struct MergeScratch {
   int32_t* run_hi;      // [K]  one past the last
   int32_t* run_cbase;   // [K+1] first partial-sum chunk of each run
   int64_t* counters;    // [8]  n_alive, merges this round, runs, chunks, next n_alive
+  int32_t* Kd;          // [1]  K, the total clip count (written by k3_video_table_kernel)
   int64_t* vstate;      // [nv][4] done, rounds, band hits, merges this round (+ alive via vstate2)
   int64_t* valive;      // [nv] alive boundaries of the video after the round
 };
 
-cudaError_t k3_prepare_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, const int32_t* cuts,
-                              MergeScratch s, cudaStream_t stream);
+// Device-side sizing: K (the clip count) and the piece count exist only on the
+// device (s.Kd, piece_base[K]); the host passes upper bounds (Kub >= K, from the
+// minimum clip length) for grids and scratch.  d_ncuts: K2's per-video cut
+// counts (the video table's n_clips / clip_base are filled from them), or null
+// when the host filled n_clips.
+cudaError_t k3_prepare_launch(MergeVideo* d_mv, int32_t nv, int32_t Kub, const int32_t* d_ncuts,
+                              const int32_t* cuts, MergeScratch s, cudaStream_t stream);
 // stride: O8' keyframe stride (1 = every frame)
-cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim,
-                                int64_t pieces_bound, int32_t stride, MergeScratch s,
-                                cudaStream_t stream);
-cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStream_t stream);
+cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t dim, int64_t pieces_bound,
+                                int32_t stride, MergeScratch s, cudaStream_t stream);
+cudaError_t k3_clip_sum_launch(int32_t Kub, int32_t dim, MergeScratch s, cudaStream_t stream);
 // every merge round of every video on the device (one cooperative launch; the
 // alive list ends in s.alive, its length in s.counters[0]); max_alive bounds
 // the boundaries (grid size); max_rounds 0 = until the fixed point.
-cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim, int64_t max_alive,
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
                              double theta, double band_rel, int32_t max_rounds, int sm_count,
                              MergeScratch s, cudaStream_t stream);
 // final cuts per video at cuts-array layout (offset cut_base, count n_final[v])
 // and the per-detected-cut cosines (same layout), from the alive list.
-cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, MergeScratch s,
+cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t Kub, MergeScratch s,
                              int32_t* final_cuts, int32_t* n_final, double* detected_cos,
                              cudaStream_t stream);
 

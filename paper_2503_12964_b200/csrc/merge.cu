@@ -43,27 +43,6 @@ __device__ __forceinline__ int32_t find_clip_video(const MergeVideo* __restrict_
   return lo;
 }
 
-// clip tables + per-video state reset
-__global__ void k3_clip_table_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K,
-                                     const int32_t* __restrict__ cuts, MergeScratch s) {
-  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < nv) {
-    int64_t* vs = s.vstate + 4 * k;
-    vs[VS_DONE] = mv[k].n_clips < 2;
-    vs[VS_ROUNDS] = 0;
-    vs[VS_BAND] = 0;
-    vs[VS_MERGES] = 0;
-    s.valive[k] = mv[k].n_clips - 1;
-  }
-  if (k >= K) return;
-  const int32_t v = find_clip_video(mv, nv, k);
-  const MergeVideo m = mv[v];
-  const int32_t j = k - m.clip_base;
-  s.clip_video[k] = v;
-  s.clip_f0[k] = j == 0 ? 0 : cuts[m.cut_base + j - 1];
-  s.clip_f1[k] = j == m.n_clips - 1 ? (int32_t)m.n : cuts[m.cut_base + j];
-}
-
 // Block-wide exclusive scan helper (any multiple of 32 threads up to 1024).
 __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* wsum, int32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -91,11 +70,59 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* wsum, int
   return r;
 }
 
+// Per-video clip counts and clip bases (ncuts: the detected-cut counts K2 left
+// on the device, or null when the host already filled them) and the total clip
+// count K (s.Kd): nothing goes back to the host between K2 and K3.
+__global__ void __launch_bounds__(1024)
+k3_video_table_kernel(MergeVideo* __restrict__ mv, int32_t nv, const int32_t* __restrict__ ncuts,
+                      MergeScratch s) {
+  __shared__ int32_t wsum[33];
+  int32_t carry = 0;
+  for (int32_t base = 0; base < nv; base += 1024) {
+    const int32_t v = base + threadIdx.x;
+    int32_t nc = 0;
+    if (v < nv) nc = ncuts ? ncuts[v] + 1 : mv[v].n_clips;
+    int32_t tot;
+    const int32_t e = block_excl_scan(nc, wsum, tot);
+    if (v < nv) {
+      mv[v].n_clips = nc;
+      mv[v].clip_base = carry + e;
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *s.Kd = carry;
+}
+
+// clip tables + per-video state reset (grid: an upper bound of K clips)
+__global__ void k3_clip_table_kernel(const MergeVideo* __restrict__ mv, int32_t nv,
+                                     const int32_t* __restrict__ cuts, MergeScratch s) {
+  const int32_t K = *s.Kd;
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  CD_CHECK(K <= (int64_t)gridDim.x * blockDim.x);  // K2's cuts obey the min clip length
+  if (k < nv) {
+    int64_t* vs = s.vstate + 4 * k;
+    vs[VS_DONE] = mv[k].n_clips < 2;
+    vs[VS_ROUNDS] = 0;
+    vs[VS_BAND] = 0;
+    vs[VS_MERGES] = 0;
+    s.valive[k] = mv[k].n_clips - 1;
+  }
+  if (k >= K) return;
+  const int32_t v = find_clip_video(mv, nv, k);
+  const MergeVideo m = mv[v];
+  const int32_t j = k - m.clip_base;
+  s.clip_video[k] = v;
+  s.clip_f0[k] = j == 0 ? 0 : cuts[m.cut_base + j - 1];
+  s.clip_f1[k] = j == m.n_clips - 1 ? (int32_t)m.n : cuts[m.cut_base + j];
+}
+
+
 // piece_base = exclusive scan of ceil(len/kPieceFrames); alive = clips that
 // start a boundary (clip_f0 > 0), in order.
 __global__ void __launch_bounds__(1024)
-k3_scan_kernel(int32_t K, MergeScratch s) {
+k3_scan_kernel(MergeScratch s) {
   __shared__ int32_t wsum[33];
+  const int32_t K = *s.Kd;
   int32_t carry_p = 0, carry_a = 0;
   for (int32_t base = 0; base < K; base += 1024) {
     const int32_t k = base + threadIdx.x;
@@ -136,11 +163,9 @@ __device__ __forceinline__ int32_t find_piece_clip(const int32_t* __restrict__ p
 
 // P[p][d] = sum of frames of piece p (f64, ascending frames); float4 loads
 // when the rows allow it (D = 768: 192 threads x 4 dims)
-__global__ void __launch_bounds__(kT)
-k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, int32_t stride,
-                    MergeScratch s) {
-  const int64_t p = blockIdx.x;
-  if (p >= s.piece_base[K]) return;
+__device__ __forceinline__ void piece_sum(const MergeVideo* __restrict__ mv, int32_t dim,
+                                          int32_t stride, const MergeScratch& s, int32_t K,
+                                          int64_t p) {
   const int32_t k = find_piece_clip(s.piece_base, K, p);
   const int32_t i = (int32_t)(p - s.piece_base[k]);
   const int32_t c0 = s.clip_f0[k];
@@ -178,27 +203,41 @@ k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t K, int32_t dim, i
   }
 }
 
-// S[k][d] = sum over the clip's pieces, ascending; norm2[k] = |S_k|^2
+// one block per piece, grid-stride (the grid is sized from an upper bound of
+// the piece count: the count itself is only on the device)
+__global__ void __launch_bounds__(kT)
+k3_piece_sum_kernel(const MergeVideo* __restrict__ mv, int32_t dim, int32_t stride,
+                    MergeScratch s) {
+  const int32_t K = *s.Kd;
+  const int64_t np = s.piece_base[K];
+  for (int64_t p = blockIdx.x; p < np; p += gridDim.x) piece_sum(mv, dim, stride, s, K, p);
+}
+
+// S[k][d] = sum over the clip's pieces, ascending; norm2[k] = |S_k|^2 (one
+// block per clip, grid-stride)
 __global__ void __launch_bounds__(kT)
 k3_clip_sum_kernel(int32_t dim, MergeScratch s) {
   __shared__ double red[kT / 32];
-  const int32_t k = blockIdx.x;
-  const int32_t p0 = s.piece_base[k], p1 = s.piece_base[k + 1];
-  double n2 = 0.0;
-  for (int32_t d = threadIdx.x; d < dim; d += kT) {
-    double acc = 0.0;
-    for (int32_t p = p0; p < p1; ++p) acc += s.P[(int64_t)p * dim + d];
-    s.S[(int64_t)k * dim + d] = acc;
-    n2 += acc * acc;
-  }
+  const int32_t K = *s.Kd;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-  if (lane == 0) red[warp] = n2;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kT / 32; ++w) t += red[w];
-    s.norm2[k] = t;
+  for (int32_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const int32_t p0 = s.piece_base[k], p1 = s.piece_base[k + 1];
+    double n2 = 0.0;
+    for (int32_t d = threadIdx.x; d < dim; d += kT) {
+      double acc = 0.0;
+      for (int32_t p = p0; p < p1; ++p) acc += s.P[(int64_t)p * dim + d];
+      s.S[(int64_t)k * dim + d] = acc;
+      n2 += acc * acc;
+    }
+    for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    if (lane == 0) red[warp] = n2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kT / 32; ++w) t += red[w];
+      s.norm2[k] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -225,8 +264,10 @@ __device__ __forceinline__ int32_t left_start(const MergeVideo* __restrict__ mv,
 constexpr int kChunk = 64;
 
 __global__ void __launch_bounds__(kT)
-k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K, int32_t dim, double theta,
+k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t dim, double theta,
                  double band_rel, int32_t max_rounds, MergeScratch s) {
+  const int32_t K = *s.Kd;
+  (void)K;  // bounds of the checked build
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t wsum[33];
@@ -391,57 +432,60 @@ k3_rounds_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K, int32
   }
 }
 
-__global__ void k3_finish_kernel(const MergeVideo* __restrict__ mv, int32_t nv, int32_t K,
+__global__ void k3_finish_kernel(const MergeVideo* __restrict__ mv, int32_t nv,
                                  MergeScratch s, int32_t* __restrict__ final_cuts,
                                  int32_t* __restrict__ n_final, double* __restrict__ detected_cos) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t K = *s.Kd;
   const int64_t n_alive = s.counters[0];
-  if (i < n_alive) {
-    const int32_t rk = s.alive[i];
-    const int32_t v = s.clip_video[rk];
-    // first alive index of video v (alive is sorted by clip index, hence by video)
-    int64_t lo = 0, hi = i;
-    while (lo < hi) {
-      const int64_t m = (lo + hi) >> 1;
-      if (s.clip_video[s.alive[m]] < v) lo = m + 1; else hi = m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n_alive) {
+      const int32_t rk = s.alive[i];
+      const int32_t v = s.clip_video[rk];
+      // first alive index of video v (alive is sorted by clip index, hence by video)
+      int64_t lo = 0, hi = i;
+      while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (s.clip_video[s.alive[m]] < v) lo = m + 1; else hi = m;
+      }
+      const int64_t pos = i - lo;
+      final_cuts[mv[v].cut_base + pos] = s.clip_f0[rk];
+      if (i + 1 == n_alive || s.clip_video[s.alive[i + 1]] != v) n_final[v] = (int32_t)(pos + 1);
     }
-    const int64_t pos = i - lo;
-    final_cuts[mv[v].cut_base + pos] = s.clip_f0[rk];
-    if (i + 1 == n_alive || s.clip_video[s.alive[i + 1]] != v) n_final[v] = (int32_t)(pos + 1);
-  }
-  if (detected_cos != nullptr && i < K) {
-    const int32_t v = s.clip_video[i];
-    const int32_t j = (int32_t)i - mv[v].clip_base;
-    if (j >= 1) detected_cos[mv[v].cut_base + j - 1] = s.cos_clip[i];
+    if (detected_cos != nullptr) {
+      const int32_t v = s.clip_video[i];
+      const int32_t j = (int32_t)i - mv[v].clip_base;
+      if (j >= 1) detected_cos[mv[v].cut_base + j - 1] = s.cos_clip[i];
+    }
   }
 }
 
 }  // namespace
 
-cudaError_t k3_prepare_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, const int32_t* cuts,
-                              MergeScratch s, cudaStream_t stream) {
-  const int32_t nthreads = K > nv ? K : nv;
-  k3_clip_table_kernel<<<(nthreads + 255) / 256, 256, 0, stream>>>(d_mv, nv, K, cuts, s);
-  k3_scan_kernel<<<1, 1024, 0, stream>>>(K, s);
+cudaError_t k3_prepare_launch(MergeVideo* d_mv, int32_t nv, int32_t Kub, const int32_t* d_ncuts,
+                              const int32_t* cuts, MergeScratch s, cudaStream_t stream) {
+  k3_video_table_kernel<<<1, 1024, 0, stream>>>(d_mv, nv, d_ncuts, s);
+  const int32_t nthreads = Kub > nv ? Kub : nv;
+  k3_clip_table_kernel<<<(nthreads + 255) / 256, 256, 0, stream>>>(d_mv, nv, cuts, s);
+  k3_scan_kernel<<<1, 1024, 0, stream>>>(s);
   return cudaGetLastError();
 }
 
-cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim,
-                                int64_t pieces_bound, int32_t stride, MergeScratch s,
-                                cudaStream_t stream) {
-  (void)nv;
-  if (K <= 0 || pieces_bound <= 0) return cudaSuccess;
-  k3_piece_sum_kernel<<<(unsigned)pieces_bound, kT, 0, stream>>>(d_mv, K, dim, stride, s);
+cudaError_t k3_piece_sum_launch(const MergeVideo* d_mv, int32_t dim, int64_t pieces_bound,
+                                int32_t stride, MergeScratch s, cudaStream_t stream) {
+  if (pieces_bound <= 0) return cudaSuccess;
+  const int64_t grid = pieces_bound < kSMs * 8 ? pieces_bound : kSMs * 8;
+  k3_piece_sum_kernel<<<(unsigned)grid, kT, 0, stream>>>(d_mv, dim, stride, s);
   return cudaGetLastError();
 }
 
-cudaError_t k3_clip_sum_launch(int32_t K, int32_t dim, MergeScratch s, cudaStream_t stream) {
-  if (K <= 0) return cudaSuccess;
-  k3_clip_sum_kernel<<<K, kT, 0, stream>>>(dim, s);
+cudaError_t k3_clip_sum_launch(int32_t Kub, int32_t dim, MergeScratch s, cudaStream_t stream) {
+  if (Kub <= 0) return cudaSuccess;
+  k3_clip_sum_kernel<<<Kub < kSMs * 8 ? Kub : kSMs * 8, kT, 0, stream>>>(dim, s);
   return cudaGetLastError();
 }
 
-cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int32_t dim, int64_t max_alive,
+cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t dim, int64_t max_alive,
                              double theta, double band_rel, int32_t max_rounds, int sm_count,
                              MergeScratch s, cudaStream_t stream) {
   static int occ = 0;
@@ -454,19 +498,19 @@ cudaError_t k3_rounds_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, int3
   int64_t want = (max_alive + kT / 32 - 1) / (kT / 32);
   int64_t grid = (int64_t)sm_count * occ;
   if (want < grid) grid = want < 1 ? 1 : want;
-  void* args[] = {(void*)&d_mv, (void*)&nv, (void*)&K, (void*)&dim, (void*)&theta,
-                  (void*)&band_rel, (void*)&max_rounds, (void*)&s};
+  void* args[] = {(void*)&d_mv, (void*)&nv, (void*)&dim, (void*)&theta, (void*)&band_rel,
+                  (void*)&max_rounds, (void*)&s};
   return cudaLaunchCooperativeKernel((const void*)k3_rounds_kernel, dim3((unsigned)grid), dim3(kT),
                                      args, 0, stream);
 }
 
-cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t K, MergeScratch s,
+cudaError_t k3_finish_launch(const MergeVideo* d_mv, int32_t nv, int32_t Kub, MergeScratch s,
                              int32_t* final_cuts, int32_t* n_final, double* detected_cos,
                              cudaStream_t stream) {
   cudaMemsetAsync(n_final, 0, sizeof(int32_t) * nv, stream);
-  if (K > 0)
-    k3_finish_kernel<<<(unsigned)((K + 255) / 256), 256, 0, stream>>>(d_mv, nv, K, s, final_cuts,
-                                                                       n_final, detected_cos);
+  const int32_t grid = (Kub + 255) / 256 < kSMs * 4 ? (Kub + 255) / 256 : kSMs * 4;
+  if (grid > 0)
+    k3_finish_kernel<<<grid, 256, 0, stream>>>(d_mv, nv, s, final_cuts, n_final, detected_cos);
   return cudaGetLastError();
 }
 
