@@ -13,11 +13,58 @@ namespace {
 
 constexpr int kGenThreads = 256;
 constexpr int kPxPerThread = 16;
+constexpr int kBlockPx = kGenThreads * kPxPerThread;
+constexpr int kMaxCells = 2048;  // texture cells one block's pixels can touch (else direct)
 
+// 16 pixels of one thread, specialised on the frame's (uniform) mode and fade
+// so that synth_finish_pixel's branches fold away.  k_of(i): palette index.
+template <uint32_t MODE, bool FADE, typename KOf>
+__device__ __forceinline__ void gen16(const uint32_t (*pal)[3], uint32_t key, uint32_t p0,
+                                      uint32_t fade_w, KOf k_of, uint32_t* bytes) {
+  uint8_t* b8 = reinterpret_cast<uint8_t*>(bytes);
+#pragma unroll  // full: the 48 output bytes stay in registers
+  for (int i = 0; i < kPxPerThread; ++i) {
+    const uint32_t k = k_of(i);
+    synth_finish_pixel(pal[k][0], pal[k][1], pal[k][2], synth_noise_word(key, p0 + i), MODE,
+                       FADE ? fade_w : 256u, b8 + 3 * i);
+  }
+}
+
+template <typename KOf>
+__device__ __forceinline__ void gen16_any(const uint32_t (*pal)[3], uint32_t key, uint32_t p0,
+                                          synth_frame fr, KOf k_of, uint32_t* bytes) {
+  const bool fade = fr.fade_w != 256u;
+  switch (fr.mode) {
+    case SYNTH_MODE_NORMAL:
+      if (fade) gen16<SYNTH_MODE_NORMAL, true>(pal, key, p0, fr.fade_w, k_of, bytes);
+      else gen16<SYNTH_MODE_NORMAL, false>(pal, key, p0, fr.fade_w, k_of, bytes);
+      break;
+    case SYNTH_MODE_ROT1:
+      gen16<SYNTH_MODE_ROT1, true>(pal, key, p0, fr.fade_w, k_of, bytes);
+      break;
+    case SYNTH_MODE_ROT2:
+      gen16<SYNTH_MODE_ROT2, true>(pal, key, p0, fr.fade_w, k_of, bytes);
+      break;
+    case SYNTH_MODE_FLASH:
+      gen16<SYNTH_MODE_FLASH, true>(pal, key, p0, fr.fade_w, k_of, bytes);
+      break;
+    default:
+      gen16<SYNTH_MODE_NOISE, true>(pal, key, p0, fr.fade_w, k_of, bytes);
+      break;
+  }
+}
+
+// One CTA = kBlockPx consecutive pixels of one frame.  The texture-cell palette
+// indices those pixels need (a 64-bit hash chain each) are computed once per
+// cell by the whole CTA into shared memory; a thread's 16 pixels then need no
+// division (16 < 2 * cell: at most two cell edges) and no warp-divergent hash
+// chain.  Bytes identical to synth_pixel (the host generator; GPU test
+// test_device_generator_matches_host).
 __global__ void __launch_bounds__(kGenThreads)
 gen_frames_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t t0,
                   const synth_frame* __restrict__ frames, uint8_t* __restrict__ out) {
   __shared__ uint32_t pal[8][3];
+  __shared__ uint8_t cellk[kMaxCells];
   const int64_t f = blockIdx.y;
   const uint32_t t = (uint32_t)(t0 + f);
   const synth_frame fr = frames[t];
@@ -25,31 +72,52 @@ gen_frames_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t
     uint32_t k = threadIdx.x / 3, c = threadIdx.x % 3;
     pal[k][c] = synth_palette(seed, video, fr.scene, k, c);
   }
-  __syncthreads();
   const uint32_t npx = W * H;
-  const uint32_t p0 = (blockIdx.x * kGenThreads + threadIdx.x) * kPxPerThread;
+  const uint32_t cell = synth_cell(W);
+  const uint32_t b0 = blockIdx.x * kBlockPx;
+  const uint32_t b1 = min(b0 + kBlockPx, npx) - 1;
+  const uint32_t cy0 = (b0 / W) / cell, cy1 = (b1 / W) / cell;
+  const uint32_t ncx = (W - 1) / cell + 1, shift = t / 8u;
+  const uint32_t ncell = (cy1 - cy0 + 1) * ncx;
+  const bool tab = ncell <= (uint32_t)kMaxCells;
+  if (tab)
+    for (uint32_t c = threadIdx.x; c < ncell; c += kGenThreads)
+      cellk[c] = (uint8_t)synth_cell_index(seed, video, fr.scene, c % ncx + shift, cy0 + c / ncx);
+  __syncthreads();
+  const uint32_t p0 = b0 + threadIdx.x * kPxPerThread;
   if (p0 >= npx) return;  // npx is a multiple of 16
   const uint32_t key = synth_noise_key(seed, video, t);
-  const uint32_t cell = synth_cell(W);
   uint32_t bytes[12];
-  uint8_t* b8 = reinterpret_cast<uint8_t*>(bytes);
-  uint32_t x = p0 % W, y = p0 / W;
-  uint32_t memo_cx = 0xFFFFFFFFu, memo_cy = 0xFFFFFFFFu, memo_k = 0;
-#pragma unroll 4
-  for (int i = 0; i < kPxPerThread; ++i) {
-    uint32_t cx = x / cell + t / 8u, cy = y / cell;
-    if (cx != memo_cx || cy != memo_cy) {
-      memo_k = synth_cell_index(seed, video, fr.scene, cx, cy);
-      memo_cx = cx;
-      memo_cy = cy;
-    }
-    uint32_t word = synth_noise_word(key, p0 + i);
-    synth_finish_pixel(pal[memo_k][0], pal[memo_k][1], pal[memo_k][2], word, fr.mode, fr.fade_w,
-                       b8 + 3 * i);
-    if (++x == W) {
-      x = 0;
-      ++y;
-    }
+  const uint32_t x = p0 % W, y = p0 / W;
+  const uint32_t cx = x / cell, rx = x - cx * cell, cy = y / cell;
+  if (tab && x + kPxPerThread <= W) {
+    // one row: pixel i is in cell cx + [rx + i >= cell] + [rx + i >= 2 cell]
+    const uint8_t* row = cellk + (cy - cy0) * ncx + cx;
+    const uint32_t e1 = cell - rx, e2 = 2 * cell - rx;
+    gen16_any(pal, key, p0, fr,
+              [&](int i) { return (uint32_t)row[((uint32_t)i >= e1) + ((uint32_t)i >= e2)]; },
+              bytes);
+  } else if (tab) {
+    // the group wraps a row (W % 16 != 0)
+    const uint32_t cyn = (y + 1) / cell;
+    gen16_any(pal, key, p0, fr,
+              [&](int i) {
+                uint32_t xi = x + i, c = cy;
+                if (xi >= W) {
+                  xi -= W;
+                  c = cyn;
+                }
+                return (uint32_t)cellk[(c - cy0) * ncx + xi / cell];
+              },
+              bytes);
+  } else {
+    // the cell table did not fit
+    gen16_any(pal, key, p0, fr,
+              [&](int i) {
+                const uint32_t q = p0 + i, xi = q % W, yi = q / W;
+                return synth_cell_index(seed, video, fr.scene, xi / cell + shift, yi / cell);
+              },
+              bytes);
   }
   uint4* dst = reinterpret_cast<uint4*>(out + (size_t)f * npx * 3 + (size_t)p0 * 3);
   dst[0] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
@@ -131,10 +199,10 @@ int synth_dev_gen_frames(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, 
                          uintptr_t stream) {
   if (n <= 0) return 0;
   if ((W * H) % 16 != 0) return (int)cudaErrorInvalidValue;
-  uint32_t groups = W * H / kPxPerThread;
+  const uint32_t npx = W * H;
   for (int64_t f0 = 0; f0 < n; f0 += 65535) {
     int64_t nf = n - f0 < 65535 ? n - f0 : 65535;
-    dim3 grid((groups + kGenThreads - 1) / kGenThreads, (unsigned)nf);
+    dim3 grid((npx + kBlockPx - 1) / kBlockPx, (unsigned)nf);
     gen_frames_kernel<<<grid, kGenThreads, 0, (cudaStream_t)stream>>>(
         seed, video, W, H, t0 + f0, d_frames, d_out + (size_t)f0 * W * H * 3);
   }

@@ -39,6 +39,25 @@ def ctx(dev):
     c.close()
 
 
+@pytest.mark.gpu
+def test_device_generator_matches_host(dev):
+    """synth_dev_gen_frames (the bench's and the streamed tests' frame source)
+    writes the host generator's bytes: tiny and odd widths (one CTA spanning
+    many texture-cell rows), C1, 480p / 1080p with fades and flashes, noise
+    frames and 4K."""
+    vids = [manifest.c1_video(),
+            manifest.random_video(7, 1, 16, 4, 40, 0.75, 0.10, 0.15, 3.0),
+            manifest.random_video(7, 2, 48, 30, 40, 0.75, 0.10, 0.15, 3.0),
+            manifest.random_video(7, 5, 40, 8, 30, 0.75, 0.10, 0.15, 3.0),
+            manifest.random_video(7, 3, 854, 480, 64, 0.75, 0.10, 0.15, 3.0),
+            manifest.subsample(manifest.c3_videos()[0], 90),
+            manifest.noise_video(4, 64, 64, 8),
+            manifest.subsample(manifest.c4_videos()[0], 2)]
+    for v in vids:
+        frames, _ = _dev_video(v, dev, emb=False)
+        assert np.array_equal(frames.cpu().numpy(), synth.gen_frames(v)), (v.id, v.W, v.H)
+
+
 def _u32(t):
     return t.cpu().numpy().view(np.uint32)
 
