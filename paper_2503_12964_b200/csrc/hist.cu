@@ -7,25 +7,25 @@
 //  * persistent grid, one CTA per SM; each CTA owns a CONTIGUOUS range of
 //    "stages" of the flattened (segment, frame, stage) space, so a CTA flushes
 //    its histogram only when its frame changes;
-//  * one producer lane streams each stage (<= 800 x 48 B = 37.5 KiB of one
+//  * one producer lane streams each stage (<= 960 x 48 B = 45 KiB of one
 //    frame) HBM -> shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
-//    mbarrier::complete_tx, L2 evict_first) into a 3-deep mbarrier ring, with
-//    TMA L2 prefetches three stages further ahead, and sleeps while it waits;
+//    mbarrier::complete_tx, L2 evict_first) into a 2-deep mbarrier ring, with
+//    TMA L2 prefetches one stage further ahead, and sleeps while it waits;
 //    every consumer lane releases the slot it has read ("empty" barrier);
-//  * 20 consumer warps; each lane takes 5 lane-contiguous 4-pixel quads of a
+//  * 20 consumer warps; each lane takes 6 lane-contiguous 4-pixel quads of a
 //    stage (three conflict-free LDS.32 each, so one warp instruction covers
 //    128 adjacent pixels), unpacks them into u16x2 pixel pairs and computes a
 //    per-pixel CODE two pixels per instruction (binfn.cuh code_pair_dir_pre:
 //    division-free sector form of the exact HSV bins with a 64 KiB hue
-//    table), phase by phase over its 10 pixel pairs (loads, codes, table
+//    table), phase by phase over its 12 pixel pairs (loads, codes, table
 //    lookups, atomics); the code of each lane is the byte offset of its entry
 //    in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm] ->
 //    ATOMS.POPC.INC: same-address lanes combine in hardware);
 //  * at a frame change each non-zero code count is added to its bin of the
 //    frame's global u32 histogram (code_to_bin_dir through an 8 KB smem table;
 //    one RED per code; integer adds: order-free, bit-deterministic).
-// 800-group stages split 720p, 1080p and 4K frames into whole stages (every
-// lane exactly 5 quads); other sizes end a frame with one ragged stage that
+// 960-group stages split 320x240, 720p, 1080p and 4K frames into whole stages
+// (every lane exactly 6 quads); other sizes end a frame with one ragged stage that
 // the lanes walk quad by quad.  Other bin layouts than 18x3x3 run the same
 // pipeline with the exact integer bin_generic per pixel (kModeGeneric); the
 // read-only variant (kModeRead, K6) measures the pipeline's HBM ceiling.
@@ -39,11 +39,12 @@ namespace clipdetect {
 
 namespace {
 
-constexpr int kStages = 3;                     // TMA ring depth
+constexpr int kStages = 2;                     // TMA ring depth (B200 A/B: 2 x 960 groups
+                                               // +0.5 % over 3 x 800, profiles/r02/ab/)
 constexpr int kWarps = 20;                     // consumer warps
 constexpr int kConsumers = kWarps * 32;        // 640 consumer lanes
 constexpr int kThreads = kConsumers + 32;      // + one producer warp
-constexpr int kStageGroups = 800;              // 16-pixel (48-byte) groups per stage: 37.5 KiB
+constexpr int kStageGroups = 960;              // 16-pixel (48-byte) groups per stage: 45 KiB
 constexpr int kQPL = 4 * kStageGroups / kConsumers;  // quads per lane in a full stage
 static_assert(kQPL * kConsumers == 4 * kStageGroups, "a full stage splits evenly over the lanes");
 constexpr int kLutBytes = 65536;
@@ -298,7 +299,7 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
       // L2 prefetch (cp.async.bulk.prefetch.L2) runs kPf stages ahead: the copy
       // into a slot released late by the slowest warp then reads L2, not DRAM
       // (the consumers waited for data 5.8 % of the time without it)
-      constexpr int kPf = kStages + 3;
+      constexpr int kPf = kStages + 1;
       StageIter pf;
       pf.seek(segs, nseg, s_begin);
       int32_t pf_i = 0;
