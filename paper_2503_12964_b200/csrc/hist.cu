@@ -7,25 +7,25 @@
 //  * persistent grid, one CTA per SM; each CTA owns a CONTIGUOUS range of
 //    "stages" of the flattened (segment, frame, stage) space, so a CTA flushes
 //    its histogram only when its frame changes;
-//  * one producer lane streams each stage (<= 960 x 48 B = 45 KiB of one
+//  * one producer lane streams each stage (<= 1024 x 48 B = 48 KiB of one
 //    frame) HBM -> shared memory with a 1-D TMA bulk copy (cp.async.bulk ...
 //    mbarrier::complete_tx, L2 evict_first) into a 2-deep mbarrier ring, with
 //    TMA L2 prefetches one stage further ahead, and sleeps while it waits;
 //    every consumer lane releases the slot it has read ("empty" barrier);
-//  * 20 consumer warps; each lane takes 6 lane-contiguous 4-pixel quads of a
+//  * 16 consumer warps; each lane takes 8 lane-contiguous 4-pixel quads of a
 //    stage (three conflict-free LDS.32 each, so one warp instruction covers
 //    128 adjacent pixels), unpacks them into u16x2 pixel pairs and computes a
 //    per-pixel CODE two pixels per instruction (binfn.cuh code_pair_dir_pre:
 //    division-free sector form of the exact HSV bins with a 64 KiB hue
-//    table), phase by phase over its 12 pixel pairs (loads, codes, table
+//    table), phase by phase over its 16 pixel pairs (loads, codes, table
 //    lookups, atomics); the code of each lane is the byte offset of its entry
 //    in a CTA-shared 8192-entry code histogram (red.shared.add [r+imm] ->
 //    ATOMS.POPC.INC: same-address lanes combine in hardware);
 //  * at a frame change each non-zero code count is added to its bin of the
 //    frame's global u32 histogram (code_to_bin_dir through an 8 KB smem table;
 //    one RED per code; integer adds: order-free, bit-deterministic).
-// 960-group stages split 320x240, 720p, 1080p and 4K frames into whole stages
-// (every lane exactly 6 quads); other sizes end a frame with one ragged stage that
+// A full 1024-group stage gives every lane exactly 8 quads; a frame that is not
+// a whole number of stages (720p: 56.25) ends with one ragged stage that
 // the lanes walk quad by quad.  Other bin layouts than 18x3x3 run the same
 // pipeline with the exact integer bin_generic per pixel (kModeGeneric); the
 // read-only variant (kModeRead, K6) measures the pipeline's HBM ceiling.
@@ -39,12 +39,13 @@ namespace clipdetect {
 
 namespace {
 
-constexpr int kStages = 2;                     // TMA ring depth (B200 A/B: 2 x 960 groups
-                                               // +0.5 % over 3 x 800, profiles/r02/ab/)
-constexpr int kWarps = 20;                     // consumer warps
-constexpr int kConsumers = kWarps * 32;        // 640 consumer lanes
+constexpr int kStages = 2;                     // TMA ring depth (B200 A/B, profiles/r02/ab/:
+                                               // 16 warps x 8 quads per lane, 2 x 1024 groups
+                                               // +1.3 % over 20 x 5, 3 x 800)
+constexpr int kWarps = 16;                     // consumer warps
+constexpr int kConsumers = kWarps * 32;        // 512 consumer lanes
 constexpr int kThreads = kConsumers + 32;      // + one producer warp
-constexpr int kStageGroups = 960;              // 16-pixel (48-byte) groups per stage: 45 KiB
+constexpr int kStageGroups = 1024;             // 16-pixel (48-byte) groups per stage: 48 KiB
 constexpr int kQPL = 4 * kStageGroups / kConsumers;  // quads per lane in a full stage
 static_assert(kQPL * kConsumers == 4 * kStageGroups, "a full stage splits evenly over the lanes");
 constexpr int kLutBytes = 65536;

@@ -16,7 +16,7 @@
 //    and the R UV rows are two contiguous byte ranges, moved by two 1-D TMA
 //    bulk copies completing on one mbarrier into a 2-deep ring of 60 KiB
 //    slots;
-//  * 20 consumer warps; a work unit is a 2 x 8 pixel tile (two LDS.64 of Y,
+//  * 24 consumer warps; a work unit is a 2 x 8 pixel tile (two LDS.64 of Y,
 //    one LDS.64 of interleaved UV = 4 chroma blocks); the chroma terms are
 //    computed once per 2 x 2 block, each horizontal pixel pair is converted
 //    directly into u16x2 lanes (VIADDMNMX luma clamp, IMAD, PRMT pack,
@@ -42,7 +42,7 @@ namespace {
 
 constexpr int kNvStages = 2;
 constexpr int kNvStageBytes = 61440;  // 3 * R * W <= 61440  <=>  R * W <= 20480
-constexpr int kNvWarps = 20;
+constexpr int kNvWarps = 24;  // B200 A/B (profiles/r02/ab/): +1.0 % over 20, 16 and 28 -2 %
 constexpr int kNvConsumers = kNvWarps * 32;
 constexpr int kNvThreads = kNvConsumers + 32;
 constexpr int kNvLutBytes = 65536;
@@ -185,8 +185,8 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, uint32_t sb
 }
 
 // The consumer loop.  A stage holds nu = R * W / 8 tiles (960 at 720p, 1080p
-// and 4K) for 640 lanes: 320 lanes take two tiles and 320 one.  The lane ->
-// tile map is rotated by 64 lanes (two warps) per stage so that the one-tile
+// and 4K) for 768 lanes: 192 lanes take two tiles and 576 one.  The lane ->
+// tile map is rotated by 64 lanes (two warps) per stage so that the two-tile
 // warps move over the four schedulers instead of always being the same ones.
 template <int MODE, bool IMM>
 __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, uint32_t* sink) {
@@ -201,7 +201,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
   uint32_t xacc = 0;
   // per-step increments of the (block row, 8-column chunk) position
   int32_t cur_w = -1, wu = 1, dq = 0, dr = 0, q64 = 0, r64 = 0, q640 = 0, r640 = 0;
-  // this stage's virtual lane u0 = (tid + 64 i) mod 640 and its (block row,
+  // this stage's virtual lane u0 = (tid + 64 i) mod kNvConsumers and its (block row,
   // 8-column chunk) = divmod(u0, wu), advanced incrementally (no per-stage division)
   int32_t u0 = tid, br0 = 0, cx0 = 0;
   uint32_t slot = 0, par = 0;
@@ -251,7 +251,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
       slot = 0;
       par ^= 1u;
     }
-    // rotate the lane -> tile map by 64 lanes: u0 += 64 (mod 640)
+    // rotate the lane -> tile map by 64 lanes: u0 += 64 (mod kNvConsumers)
     u0 += 64;
     br0 += q64;
     cx0 += r64;
