@@ -633,3 +633,34 @@ def test_merge_20k_cuts_near_constant_under_5ms(ctx, dev):
     ms = float(np.median(times[1:]))
     print(f"clip_merge 20,000 cuts x 768: {ms:.3f} ms (median of 5)")
     assert ms < 5.0, times
+
+
+def test_run_videos_at_the_cut_count_bound(ctx, dev):
+    """Videos whose colour flips every L_min = 8 frames (a cut at every allowed
+    frame: the clip count K reaches the n / L_min bound the host sizes K3's
+    scratch and grids with, while K itself exists only on the device) batched
+    with a one-frame and a short video; embeddings on a random walk so merges
+    cascade over several rounds.  Every list, count and cosine against the
+    oracle."""
+    rng = np.random.default_rng(2024)
+    pal = np.array([[250, 10, 10], [10, 10, 250]], dtype=np.uint8)
+    items, refs = [], []
+    for n in [400, 301, 1, 64, 1003]:
+        host = np.ascontiguousarray(np.broadcast_to(
+            pal[(np.arange(n) // 8) % 2][:, None, None, :], (n, 16, 16, 3)))
+        phi = np.cumsum(rng.uniform(-40.0, 40.0, n // 8 + 1)) * np.pi / 180
+        e = np.zeros((n, 8), dtype=np.float32)
+        e[:, 0] = np.cos(phi[np.arange(n) // 8])
+        e[:, 1] = np.sin(phi[np.arange(n) // 8])
+        items.append({"n": n, "H": 16, "W": 16, "frames": torch.from_numpy(host).to(dev),
+                      "emb": torch.from_numpy(e).to(dev)})
+        refs.append(oracle.run_video(host, e))
+    res = ctx.run_videos(items, want_cos=True)
+    assert any(ref.rounds >= 3 for ref in refs)
+    for n, r, ref in zip([400, 301, 1, 64, 1003], res, refs):
+        c = (n - 1) // 8  # a candidate every 8 frames; the tail rule drops a last clip < 8
+        assert len(ref.detected) == c - (1 if c > 0 and n - 8 * c < 8 else 0)
+        assert list(r.detected) == list(ref.detected)
+        assert list(r.final) == list(ref.final)
+        assert r.rounds == ref.rounds and r.n_band_hits == ref.n_band_hits
+        np.testing.assert_allclose(r.detected_cos, ref.cos, rtol=COS_RTOL, atol=1e-12)
