@@ -4,7 +4,8 @@ K1 (RGB24) and K1-NV12 over the first N frames of the C2 video, K4 on the
 final clips of a 2,000-frame prefix, and the K3 merge (clip_merge) of that
 prefix.  Runs each once untimed (warm-up, module load) then once more.
 
-usage: python tools/k1_one.py [n_frames] [which: k1,nv12,k4,k3]"""
+usage: python tools/k1_one.py [n_frames] [which: k1,nv12,k4,k3,noise]
+(noise: K1 over n_frames / 4 uniform-noise 1080p frames, the worst case)"""
 import os
 import sys
 
@@ -45,6 +46,16 @@ def main():
         if "k4" in which:
             for _ in range(2):
                 ctx.sample_frames(frames, fin, 8, 224, 224, want_index=False)
+    if "noise" in which:
+        nz = manifest.noise_video(1, n=max(1, n // 4))
+        ft = torch_dev.frame_table(nz, dev)
+        nf = torch.empty((nz.n, nz.H, nz.W, 3), dtype=torch.uint8, device=dev)
+        torch_dev.gen_frames(nz, ft, nf)
+        nh = torch.empty((nz.n, 162), dtype=torch.int32, device=dev)
+        for _ in range(2):
+            ctx.frame_scores(nf, hist=nh, want_l1=False, want_score=False)
+        del nf
+        torch.cuda.empty_cache()
     if "nv12" in which:
         del frames
         torch.cuda.empty_cache()
