@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/clip_detect.h"
+#include "binfn.cuh"
 #include "kernels.cuh"
 
 using namespace clipdetect;
@@ -54,7 +55,16 @@ struct clip_ctx {
   // pinned host staging for small D2H
   void* hpin = nullptr;
   size_t hpin_bytes = 0;
+  // K1 / K1-NV12 shared-memory tables (k1_tables_build; RGB then NV12), built once
+  DevBuf tables;
+  // pinned double buffer for small H2D descriptor tables: a pageable
+  // cudaMemcpyAsync would block the host until the stream drains, so every
+  // streamed chunk's K1 launch would wait for the previous one
+  uint8_t* dpin = nullptr;
+  cudaEvent_t desc_ev[2] = {nullptr, nullptr};
+  int desc_half = 0;
 };
+constexpr size_t kDescHalf = 128 << 10;
 
 namespace {
 
@@ -84,6 +94,24 @@ int fail(clip_ctx* c, int code, const char* fmt, ...) {
     int s_ = (call);                    \
     if (s_ != CLIP_OK) return s_;       \
   } while (0)
+
+// Host -> device copy of a small descriptor table on the ctx stream through the
+// pinned double buffer (falls back to a plain copy above kDescHalf bytes).
+int upload(clip_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return CLIP_OK;
+  if (bytes > kDescHalf) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return CLIP_OK;
+  }
+  const int h = ctx->desc_half;
+  ctx->desc_half ^= 1;
+  CK(cudaEventSynchronize(ctx->desc_ev[h]));  // the copy that last used this half is done
+  uint8_t* stage = ctx->dpin + h * kDescHalf;
+  memcpy(stage, src, bytes);
+  CK(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->desc_ev[h], ctx->stream));
+  return CLIP_OK;
+}
 
 int ensure(clip_ctx* ctx, DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
@@ -194,12 +222,12 @@ int launch_k1(clip_ctx* ctx, std::vector<HistSeg>& segs, int mode) {
   }
   if (total == 0) return CLIP_OK;
   CKS(ensure(ctx, ctx->segs, segs.size() * sizeof(HistSeg)));
-  CK(cudaMemcpyAsync(ctx->segs.p, segs.data(), segs.size() * sizeof(HistSeg),
-                     cudaMemcpyHostToDevice, ctx->stream));
+  CKS(upload(ctx, ctx->segs.p, segs.data(), segs.size() * sizeof(HistSeg)));
   CKS(ensure(ctx, ctx->sink, 16));
   Span sp(ctx, 0);
   CK(k1_launch(mode, P<HistSeg>(ctx->segs), (int32_t)segs.size(), total, ctx->p.h_bins,
-               ctx->p.s_bins, ctx->p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count, ctx->stream));
+               ctx->p.s_bins, ctx->p.v_bins, P<uint8_t>(ctx->tables), P<uint32_t>(ctx->sink),
+               ctx->sm_count, ctx->stream));
   sp.end();
   ctx->stats.k1_launches += 1;
   ctx->stats.launches += 1;
@@ -229,13 +257,12 @@ int launch_k1_nv12(clip_ctx* ctx, const std::vector<Nv12Seg>& all, int mode) {
     }
     CKS(ensure(ctx, k ? ctx->segs2 : ctx->segs, segs.size() * sizeof(Nv12Seg)));
     DevBuf& db = k ? ctx->segs2 : ctx->segs;
-    CK(cudaMemcpyAsync(db.p, segs.data(), segs.size() * sizeof(Nv12Seg), cudaMemcpyHostToDevice,
-                       ctx->stream));
+    CKS(upload(ctx, db.p, segs.data(), segs.size() * sizeof(Nv12Seg)));
     CKS(ensure(ctx, ctx->sink, 16));
     Span sp(ctx, 0);
     CK(k1_nv12_launch(k ? kModeGeneric : mode, P<Nv12Seg>(db), (int32_t)segs.size(), total,
-                      p.h_bins, p.s_bins, p.v_bins, P<uint32_t>(ctx->sink), ctx->sm_count,
-                      ctx->stream));
+                      p.h_bins, p.s_bins, p.v_bins, P<uint8_t>(ctx->tables) + kK1TableBytes,
+                      P<uint32_t>(ctx->sink), ctx->sm_count, ctx->stream));
     sp.end();
     ctx->stats.k1_launches += 1;
     ctx->stats.launches += 1;
@@ -329,8 +356,7 @@ int run_merge(clip_ctx* ctx, const std::vector<MergeVideo>& mvh, int32_t dim, co
   CKS(ensure(ctx, ctx->m_counters, 8 * 9));
   CKS(ensure(ctx, ctx->m_vstate, 8 * 4 * nv));
   CKS(ensure(ctx, ctx->m_valive, 8 * nv));
-  CK(cudaMemcpyAsync(ctx->m_video.p, mvh.data(), sizeof(MergeVideo) * nv, cudaMemcpyHostToDevice,
-                     ctx->stream));
+  CKS(upload(ctx, ctx->m_video.p, mvh.data(), sizeof(MergeVideo) * nv));
   CK(cudaMemsetAsync(ctx->m_cos_clip.p, 0, 8 * K, ctx->stream));
   MergeScratch s;
   s.clip_video = P<int32_t>(ctx->m_clip_video);
@@ -493,6 +519,17 @@ int clip_detect_init(clip_ctx** out, const clip_params* p, int cuda_device, uint
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&ctx->copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->consumed[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->desc_ev[i], cudaEventDisableTiming);
+  }
+  // the fast paths' shared-memory tables, once per context
+  if (cudaMallocHost(reinterpret_cast<void**>(&ctx->dpin), 2 * kDescHalf) != cudaSuccess ||
+      ensure(ctx, ctx->tables, 2 * kK1TableBytes) != CLIP_OK ||
+      k1_tables_build(P<uint8_t>(ctx->tables), kHashRgb, ctx->stream) != cudaSuccess ||
+      k1_tables_build(P<uint8_t>(ctx->tables) + kK1TableBytes, kHashNv12, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    clip_detect_destroy(ctx);
+    return CLIP_E_CUDA;
   }
   *out = ctx;
   return CLIP_OK;
@@ -509,14 +546,16 @@ int clip_detect_destroy(clip_ctx* ctx) {
                     &ctx->m_piece_base, &ctx->m_P, &ctx->m_S, &ctx->m_alive, &ctx->m_alive2,
                     &ctx->m_cos_b, &ctx->m_cos_clip, &ctx->m_norm2, &ctx->m_runs,
                     &ctx->m_counters, &ctx->m_vstate,
-                    &ctx->m_valive, &ctx->staging[0], &ctx->staging[1]};
+                    &ctx->m_valive, &ctx->staging[0], &ctx->staging[1], &ctx->tables};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (ctx->copied[i]) cudaEventDestroy(ctx->copied[i]);
     if (ctx->consumed[i]) cudaEventDestroy(ctx->consumed[i]);
+    if (ctx->desc_ev[i]) cudaEventDestroy(ctx->desc_ev[i]);
   }
+  if (ctx->dpin) cudaFreeHost(ctx->dpin);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   delete ctx;
@@ -552,7 +591,7 @@ int frame_scores(clip_ctx* ctx, int format, const uint8_t* frames, int64_t n_fra
   if (l1 || score) {
     VideoDesc vd{0, n_frames, npix};
     CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
-    CK(cudaMemcpyAsync(ctx->vids.p, &vd, sizeof vd, cudaMemcpyHostToDevice, ctx->stream));
+    CKS(upload(ctx, ctx->vids.p, &vd, sizeof vd));
     Span sp(ctx, 1);
     const bool var = ctx->p.distance != CLIP_DIST_L1;
     CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1,
@@ -597,7 +636,7 @@ int clip_hist_scores(clip_ctx* ctx, const uint32_t* hist, int64_t n_frames, int6
   const uint32_t nbins = nbins_of(ctx->p);
   VideoDesc vd{0, n_frames, pixels_per_frame};
   CKS(ensure(ctx, ctx->vids, sizeof(VideoDesc)));
-  CK(cudaMemcpyAsync(ctx->vids.p, &vd, sizeof vd, cudaMemcpyHostToDevice, ctx->stream));
+  CKS(upload(ctx, ctx->vids.p, &vd, sizeof vd));
   Span sp(ctx, 1);
   const bool var = ctx->p.distance != CLIP_DIST_L1;
   CK(k2_l1_launch(hist, n_frames, P<VideoDesc>(ctx->vids), 1, nbins, prev_hist, l1,
@@ -735,8 +774,7 @@ int clip_run_videos(clip_ctx* ctx, const clip_video* videos, int32_t n_videos, c
   CKS(ensure(ctx, ctx->detcos, 8 * F));
 
   Span whole(ctx, 3);
-  CK(cudaMemcpyAsync(ctx->vids.p, vd.data(), sizeof(VideoDesc) * n_videos, cudaMemcpyHostToDevice,
-                     ctx->stream));
+  CKS(upload(ctx, ctx->vids.p, vd.data(), sizeof(VideoDesc) * n_videos));
   CK(cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * nbins * F, ctx->stream));
 
   // ---- K1: device-resident videos in one launch

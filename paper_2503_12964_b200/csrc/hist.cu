@@ -62,6 +62,7 @@ struct K1Smem {
   uint8_t c2b[kDirCodes];    // code -> bin
   uint64_t full[kStages];
   uint64_t empty[kStages];
+  uint64_t tab;  // the lut + c2b bulk copy at launch
   MadK mk;
   int32_t seq[kStages];  // checked builds: the stage index the producer put in each slot
 };
@@ -206,6 +207,7 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const His
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t xacc = 0;
+  if constexpr (MODE == kModeFast) mbar_wait(&sm.tab, 0);  // the tables have landed
   StageIter it;
   it.seek(segs, nseg, s_begin);
   uint32_t slot = 0, par = 0;
@@ -261,7 +263,8 @@ __device__ __forceinline__ void k1_consume(K1Smem& sm, uint32_t sbase, const His
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_stages,
-               uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param, uint32_t* __restrict__ sink) {
+               uint32_t nh, uint32_t ns, uint32_t nv, MadK mk_param,
+               const uint8_t* __restrict__ tables, uint32_t* __restrict__ sink) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -272,23 +275,27 @@ k1_hist_kernel(const HistSeg* __restrict__ segs, int32_t nseg, int64_t total_sta
   if (MODE != kModeRead) {
     for (int i = tid; i < kDirCodes; i += kThreads) sm.hist[i] = 0u;
   }
-  if (MODE == kModeFast) {
-    for (int i = tid; i < kDirCodes; i += kThreads) sm.c2b[i] = (uint8_t)code_to_bin_dir(i);
-    for (int i = tid; i < kLutBytes; i += kThreads) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d);
-      sm.lut[i] = (uint8_t)(na > d ? 0u : lut_entry_dir(na, d, kHashRgb));
-    }
-  }
   if (tid == 0) {
     sm.mk = mk_param;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], kConsumers);
     }
+    mbar_init(&sm.tab, 1);
     fence_mbar_init();
+    if (MODE == kModeFast) {  // hue table and code -> bin map: one bulk copy each
+      CD_CHECK(tables != nullptr && (reinterpret_cast<uintptr_t>(tables) & 15) == 0);
+      const uint64_t pol = policy_evict_last();
+      mbar_arrive_expect_tx(&sm.tab, kLutBytes + kDirCodes);
+      bulk_g2s(sm.lut, tables, kLutBytes, &sm.tab, pol);
+      bulk_g2s(sm.c2b, tables + kLutBytes, kDirCodes, &sm.tab, pol);
+    }
   }
   __syncthreads();
-  if (s_begin >= s_end) return;
+  if (s_begin >= s_end) {
+    if (MODE == kModeFast && tid == 0) mbar_wait(&sm.tab, 0);  // no copy outlives the CTA
+    return;
+  }
   const int32_t n = (int32_t)(s_end - s_begin);
 
   if (warp == kWarps) {
@@ -362,21 +369,42 @@ cudaError_t k1_configure() {
                               (int)sizeof(K1Smem));
 }
 
+namespace {
+__global__ void k1_tables_kernel(uint8_t* __restrict__ t, int hash) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutBytes + kDirCodes;
+       i += gridDim.x * blockDim.x) {
+    if (i < kLutBytes) {
+      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d);
+      t[i] = (uint8_t)(na > d ? 0u : lut_entry_dir(na, d, hash));
+    } else {
+      t[i] = (uint8_t)code_to_bin_dir((uint32_t)(i - kLutBytes));
+    }
+  }
+}
+}  // namespace
+
+static_assert(kK1TableBytes == kLutBytes + kDirCodes, "table layout");
+
+cudaError_t k1_tables_build(uint8_t* d_tables, int hash, cudaStream_t stream) {
+  k1_tables_kernel<<<kSMs, 256, 0, stream>>>(d_tables, hash);
+  return cudaGetLastError();
+}
+
 cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
-                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                      cudaStream_t stream) {
+                      uint32_t nh, uint32_t ns, uint32_t nv, const uint8_t* tables,
+                      uint32_t* sink, int sm_count, cudaStream_t stream) {
   if (total_stages <= 0) return cudaSuccess;
   const int grid = (int)(total_stages < sm_count ? total_stages : sm_count);
   const size_t smem = sizeof(K1Smem);
   if (mode == kModeFast)
     k1_hist_kernel<kModeFast><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh, ns,
-                                                                nv, kMadK, sink);
+                                                                nv, kMadK, tables, sink);
   else if (mode == kModeGeneric)
     k1_hist_kernel<kModeGeneric><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh,
-                                                                   ns, nv, kMadK, sink);
+                                                                   ns, nv, kMadK, tables, sink);
   else
     k1_hist_kernel<kModeRead><<<grid, kThreads, smem, stream>>>(d_segs, nseg, total_stages, nh, ns,
-                                                                nv, kMadK, sink);
+                                                                nv, kMadK, tables, sink);
   return cudaGetLastError();
 }
 

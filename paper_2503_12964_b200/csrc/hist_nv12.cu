@@ -67,6 +67,7 @@ struct NvSmem {
   uint8_t c2b[kDirCodes];
   uint64_t full[kNvStages];
   uint64_t empty[kNvStages];
+  uint64_t tab;  // the lut + c2b bulk copies at launch
   MadK mk;
 };
 constexpr uint32_t kNvLutOff = (uint32_t)offsetof(NvSmem, lut);
@@ -199,6 +200,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
     for (int j = 0; j < (int)(sizeof(MadK) / 4); ++j) m[j] = v[j];
   }
   uint32_t xacc = 0;
+  if constexpr (MODE == kModeFast) mbar_wait(&sm.tab, 0);  // the tables have landed
   // per-step increments of the (block row, 8-column chunk) position
   int32_t cur_w = -1, wu = 1, dq = 0, dr = 0, q64 = 0, r64 = 0, q640 = 0, r640 = 0;
   // this stage's virtual lane u0 = (tid + 64 i) mod kNvConsumers and its (block row,
@@ -289,7 +291,7 @@ __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, u
 template <int MODE>
 __global__ void __launch_bounds__(kNvThreads, 1)
 k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_stages,
-               MadK mk_param, uint32_t* __restrict__ sink) {
+               MadK mk_param, const uint8_t* __restrict__ tables, uint32_t* __restrict__ sink) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   NvSmem& sm = *reinterpret_cast<NvSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -298,14 +300,7 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
   const int64_t s_end = total_stages * (blockIdx.x + 1) / gridDim.x;
 
   if (MODE == kModeFast) {
-    for (int i = tid; i < kDirCodes; i += kNvThreads) {
-      sm.hist[i] = 0u;
-      sm.c2b[i] = (uint8_t)code_to_bin_dir(i);
-    }
-    for (int i = tid; i < kNvLutBytes; i += kNvThreads) {
-      const uint32_t d = (uint32_t)i >> 8, na = lut_unswizzle((uint32_t)i & 255u, d);
-      sm.lut[i] = (uint8_t)(na > d ? 0u : lut_entry_dir(na, d, kHashNv12));
-    }
+    for (int i = tid; i < kDirCodes; i += kNvThreads) sm.hist[i] = 0u;
   }
   if (tid == 0) {
     sm.mk = mk_param;
@@ -313,10 +308,21 @@ k1_nv12_kernel(const Nv12Seg* __restrict__ segs, int32_t nseg, int64_t total_sta
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], kNvConsumers);
     }
+    mbar_init(&sm.tab, 1);
     fence_mbar_init();
+    if (MODE == kModeFast) {  // hue table and code -> bin map (k1_tables_build, kHashNv12)
+      CD_CHECK(tables != nullptr && (reinterpret_cast<uintptr_t>(tables) & 15) == 0);
+      const uint64_t pol = policy_evict_last();
+      mbar_arrive_expect_tx(&sm.tab, kNvLutBytes + kDirCodes);
+      bulk_g2s(sm.lut, tables, kNvLutBytes, &sm.tab, pol);
+      bulk_g2s(sm.c2b, tables + kNvLutBytes, kDirCodes, &sm.tab, pol);
+    }
   }
   __syncthreads();
-  if (s_begin >= s_end) return;
+  if (s_begin >= s_end) {
+    if (MODE == kModeFast && tid == 0) mbar_wait(&sm.tab, 0);  // no copy outlives the CTA
+    return;
+  }
   const int32_t n = (int32_t)(s_end - s_begin);
 
   if (warp == kNvWarps) {
@@ -468,8 +474,8 @@ cudaError_t k1_nv12_configure() {
 }
 
 cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
-                           uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                           cudaStream_t stream) {
+                           uint32_t nh, uint32_t ns, uint32_t nv, const uint8_t* tables,
+                           uint32_t* sink, int sm_count, cudaStream_t stream) {
   if (total <= 0) return cudaSuccess;
   if (mode == kModeGeneric) {
     const int64_t grid = std::min<int64_t>(total, (int64_t)sm_count * 8);
@@ -478,9 +484,11 @@ cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_
   }
   const int grid = (int)std::min<int64_t>(total, sm_count);
   if (mode == kModeFast)
-    k1_nv12_kernel<kModeFast><<<grid, kNvThreads, sizeof(NvSmem), stream>>>(d_segs, nseg, total, kMadK, sink);
+    k1_nv12_kernel<kModeFast><<<grid, kNvThreads, sizeof(NvSmem), stream>>>(d_segs, nseg, total, kMadK,
+                                                                          tables, sink);
   else
-    k1_nv12_kernel<kModeRead><<<grid, kNvThreads, sizeof(NvSmem), stream>>>(d_segs, nseg, total, kMadK, sink);
+    k1_nv12_kernel<kModeRead><<<grid, kNvThreads, sizeof(NvSmem), stream>>>(d_segs, nseg, total, kMadK,
+                                                                          tables, sink);
   return cudaGetLastError();
 }
 

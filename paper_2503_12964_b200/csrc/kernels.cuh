@@ -13,10 +13,16 @@ enum { kModeFast = 0, kModeGeneric = 1, kModeRead = 2 };
 // ---- K1 (hist.cu)
 int64_t k1_stages(int64_t groups);  // K1 stages of a frame of `groups` 48-byte groups
 cudaError_t k1_configure();
-// persistent grid of min(total_stages, sm_count) CTAs
+// The fast path's shared-memory tables, built once per context into global
+// memory (kK1TableBytes each: the 64 KiB hue table, then the 8 KiB code -> bin
+// map) and moved into every CTA by one TMA bulk copy at launch instead of
+// being recomputed per CTA per launch.  hash: kHashRgb (K1) or kHashNv12.
+constexpr int kK1TableBytes = 65536 + 8192;
+cudaError_t k1_tables_build(uint8_t* d_tables, int hash, cudaStream_t stream);
+// persistent grid of min(total_stages, sm_count) CTAs; tables: k1_tables_build(kHashRgb)
 cudaError_t k1_launch(int mode, const HistSeg* d_segs, int32_t nseg, int64_t total_stages,
-                      uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                      cudaStream_t stream);
+                      uint32_t nh, uint32_t ns, uint32_t nv, const uint8_t* tables,
+                      uint32_t* sink, int sm_count, cudaStream_t stream);
 cudaError_t k5_binmap_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                              cudaStream_t stream);
 
@@ -27,9 +33,10 @@ int nv12_generic_rows();
 cudaError_t k1_nv12_configure();
 // mode kModeFast / kModeRead: persistent TMA kernel over `total` stages;
 // kModeGeneric: generic kernel over `total` (frame, 8-block-row) items.
+// tables: k1_tables_build(kHashNv12)
 cudaError_t k1_nv12_launch(int mode, const Nv12Seg* d_segs, int32_t nseg, int64_t total,
-                           uint32_t nh, uint32_t ns, uint32_t nv, uint32_t* sink, int sm_count,
-                           cudaStream_t stream);
+                           uint32_t nh, uint32_t ns, uint32_t nv, const uint8_t* tables,
+                           uint32_t* sink, int sm_count, cudaStream_t stream);
 cudaError_t k5_nv12map_launch(uint8_t* out, uint32_t nh, uint32_t ns, uint32_t nv, int fast,
                               cudaStream_t stream);
 
