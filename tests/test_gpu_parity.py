@@ -664,3 +664,28 @@ def test_run_videos_at_the_cut_count_bound(ctx, dev):
         assert list(r.final) == list(ref.final)
         assert r.rounds == ref.rounds and r.n_band_hits == ref.n_band_hits
         np.testing.assert_allclose(r.detected_cos, ref.cos, rtol=COS_RTOL, atol=1e-12)
+
+
+def test_run_videos_thousands_of_tiny_videos(ctx, dev):
+    """3,000 device-resident 16x16 videos in one call: more segment descriptors
+    than the pinned upload buffer holds (the plain-copy fallback), and the
+    device-side video-table and summary scans over several 1,024-video blocks.
+    Every video's lists against the oracle."""
+    rng = np.random.default_rng(9)
+    n_vid, n = 3000, 24
+    pal = rng.integers(0, 256, size=(n_vid, 3, 3), dtype=np.uint8)
+    change = rng.integers(8, 17, size=n_vid)
+    host = np.empty((n_vid, n, 16, 16, 3), dtype=np.uint8)
+    for i in range(n_vid):
+        idx = (np.arange(n) >= change[i]).astype(int) + (np.arange(n) >= change[i] + 8).astype(int)
+        host[i] = pal[i][idx][:, None, None, :]
+    emb = rng.standard_normal((n_vid, n, 8)).astype(np.float32)
+    fr = torch.from_numpy(host).to(dev)
+    ed = torch.from_numpy(emb).to(dev)
+    items = [{"n": n, "H": 16, "W": 16, "frames": fr[i], "emb": ed[i], "id": i} for i in range(n_vid)]
+    res = ctx.run_videos(items, want_cos=True)
+    for i in range(0, n_vid, 7):
+        ref = oracle.run_video(host[i], emb[i])
+        assert list(res[i].detected) == list(ref.detected), i
+        assert list(res[i].final) == list(ref.final), i
+    assert sum(len(r.detected) for r in res) > 0
