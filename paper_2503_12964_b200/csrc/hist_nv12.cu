@@ -185,10 +185,11 @@ __device__ __forceinline__ void nv_tile(uint2 y0, uint2 y1, uint2 c, uint32_t sb
   }
 }
 
-// The consumer loop.  A stage holds nu = R * W / 8 tiles (960 at 720p, 1080p
-// and 4K) for 768 lanes: 192 lanes take two tiles and 576 one.  The lane ->
-// tile map is rotated by 64 lanes (two warps) per stage so that the two-tile
-// warps move over the four schedulers instead of always being the same ones.
+// The consumer loop.  A stage holds nu = R * W / 8 tiles (2,560 at 720p, 2,400
+// at 1080p and 4K) for 768 lanes: at 720p 256 lanes take four tiles and 512
+// three.  The lane -> tile map is rotated by 64 lanes (two warps) per stage so
+// that the lanes with the extra tile move over the four schedulers instead of
+// always being the same ones.
 template <int MODE, bool IMM>
 __device__ __forceinline__ void nv_consume(NvSmem& sm, uint32_t sb, int32_t n, uint32_t* sink) {
   const int tid = threadIdx.x;
