@@ -65,20 +65,28 @@ gen_frames_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t
                   const synth_frame* __restrict__ frames, uint8_t* __restrict__ out) {
   __shared__ uint32_t pal[8][3];
   __shared__ uint8_t cellk[kMaxCells];
+  __shared__ uint32_t u_key, u_cy0, u_ncx, u_ncell, u_x0, u_y0;  // CTA-uniform, computed once
   const int64_t f = blockIdx.y;
   const uint32_t t = (uint32_t)(t0 + f);
   const synth_frame fr = frames[t];
-  if (threadIdx.x < 24) {
-    uint32_t k = threadIdx.x / 3, c = threadIdx.x % 3;
-    pal[k][c] = synth_palette(seed, video, fr.scene, k, c);
-  }
   const uint32_t npx = W * H;
   const uint32_t cell = synth_cell(W);
   const uint32_t b0 = blockIdx.x * kBlockPx;
-  const uint32_t b1 = min(b0 + kBlockPx, npx) - 1;
-  const uint32_t cy0 = (b0 / W) / cell, cy1 = (b1 / W) / cell;
-  const uint32_t ncx = (W - 1) / cell + 1, shift = t / 8u;
-  const uint32_t ncell = (cy1 - cy0 + 1) * ncx;
+  if (threadIdx.x == 0) {
+    const uint32_t b1 = min(b0 + kBlockPx, npx) - 1;
+    u_x0 = b0 % W;
+    u_y0 = b0 / W;
+    u_cy0 = u_y0 / cell;
+    u_ncx = (W - 1) / cell + 1;
+    u_ncell = ((b1 / W) / cell - u_cy0 + 1) * u_ncx;
+  } else if (threadIdx.x == 32) {
+    u_key = synth_noise_key(seed, video, t);
+  } else if (threadIdx.x >= 64 && threadIdx.x < 64 + 24) {
+    const uint32_t k = (threadIdx.x - 64) / 3, c = (threadIdx.x - 64) % 3;
+    pal[k][c] = synth_palette(seed, video, fr.scene, k, c);
+  }
+  __syncthreads();
+  const uint32_t cy0 = u_cy0, ncx = u_ncx, ncell = u_ncell, shift = t / 8u;
   const bool tab = ncell <= (uint32_t)kMaxCells;
   if (tab)
     for (uint32_t c = threadIdx.x; c < ncell; c += kGenThreads)
@@ -86,9 +94,19 @@ gen_frames_kernel(uint64_t seed, uint32_t video, uint32_t W, uint32_t H, int64_t
   __syncthreads();
   const uint32_t p0 = b0 + threadIdx.x * kPxPerThread;
   if (p0 >= npx) return;  // npx is a multiple of 16
-  const uint32_t key = synth_noise_key(seed, video, t);
+  const uint32_t key = u_key;
   uint32_t bytes[12];
-  const uint32_t x = p0 % W, y = p0 / W;
+  // (x, y) of p0 from the CTA's first pixel without a per-thread division
+  uint32_t x = u_x0 + threadIdx.x * kPxPerThread, y = u_y0;
+  if (W >= 256) {
+    while (x >= W) {
+      x -= W;
+      ++y;
+    }
+  } else {
+    y += x / W;
+    x %= W;
+  }
   const uint32_t cx = x / cell, rx = x - cx * cell, cy = y / cell;
   if (tab && x + kPxPerThread <= W) {
     // one row: pixel i is in cell cx + [rx + i >= cell] + [rx + i >= 2 cell]
