@@ -114,31 +114,45 @@ __global__ void k2_greedy_kernel(const VideoDesc* __restrict__ vids, int32_t nvi
   int32_t* out = cuts + fbase;  // capacity n per video
   int64_t last = 0;
   int32_t k = 0, nc = 0;
+  auto take = [&](int64_t f) {  // the greedy step for candidate frame f (ascending)
+    if (f < fbase || f >= fbase + n) return;
+    const int64_t t = f - fbase;
+    ++nc;
+    if (t - last >= l_min) {
+      CD_CHECK(k < n && t > last);  // cuts strictly increasing, capacity n per video
+      if (lane == 0) out[k] = (int32_t)t;
+      ++k;
+      last = t;
+    }
+  };
+  constexpr int kPre = 4;  // candidates per chunk fetched up front, all chunks at once
   for (int64_t cb = c0; cb <= c1; cb += 32) {
     const int64_t c = cb + lane;
     const int32_t cnt = c <= c1 ? cand_count[c] : 0;
     CD_CHECK(cnt >= 0 && cnt <= kCompactFrames);
+    // every lane loads the first kPre candidates of its chunk: one round trip
+    // for the 32 chunks instead of one per non-empty chunk
+    int32_t pre[kPre];
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) pre[j] = j < cnt ? cand_slots[c * kCompactFrames + j] : -1;
     uint32_t nz = __ballot_sync(0xffffffffu, cnt > 0);
     while (nz) {
       const int src = __ffs(nz) - 1;
       nz &= nz - 1;
       const int32_t cc = __shfl_sync(0xffffffffu, cnt, src);
       const int64_t chunk = cb + src;
+      if (cc <= kPre) {
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) {
+          const int32_t f = __shfl_sync(0xffffffffu, pre[j], src);
+          if (j < cc) take(f);
+        }
+        continue;
+      }
       for (int32_t e0 = 0; e0 < cc; e0 += 32) {
         const int32_t fidx = e0 + lane < cc ? cand_slots[chunk * kCompactFrames + e0 + lane] : -1;
         const int32_t m = min(32, cc - e0);
-        for (int32_t i = 0; i < m; ++i) {
-          const int64_t f = __shfl_sync(0xffffffffu, fidx, i);
-          if (f < fbase || f >= fbase + n) continue;
-          const int64_t t = f - fbase;
-          ++nc;
-          if (t - last >= l_min) {
-            CD_CHECK(k < n && t > last);  // cuts strictly increasing, capacity n per video
-            if (lane == 0) out[k] = (int32_t)t;
-            ++k;
-            last = t;
-          }
-        }
+        for (int32_t i = 0; i < m; ++i) take(__shfl_sync(0xffffffffu, fidx, i));
       }
     }
   }
