@@ -689,3 +689,31 @@ def test_run_videos_thousands_of_tiny_videos(ctx, dev):
         assert list(res[i].detected) == list(ref.detected), i
         assert list(res[i].final) == list(ref.final), i
     assert sum(len(r.detected) for r in res) > 0
+
+
+def test_run_videos_every_frame_a_candidate(ctx, dev):
+    """Colours alternating every frame: every frame t >= 1 is a candidate, so
+    every 128-frame compaction chunk is full (K2's greedy takes its per-chunk
+    path, not the four-candidate prefetch) and the greedy keeps every L_min-th
+    frame: detected = {8, 16, ...} by the closed form, and equal to the oracle,
+    for two videos batched with a sparse one."""
+    pal = np.array([[250, 10, 10], [10, 10, 250]], dtype=np.uint8)
+    items, refs, ns = [], [], [1000, 259, 333]
+    rng = np.random.default_rng(5)
+    for vi, n in enumerate(ns):
+        idx = np.arange(n) % 2 if vi != 1 else (np.arange(n) // 37) % 2
+        host = np.ascontiguousarray(np.broadcast_to(pal[idx][:, None, None, :], (n, 16, 16, 3)))
+        e = rng.standard_normal((n, 8)).astype(np.float32)
+        items.append({"n": n, "H": 16, "W": 16, "frames": torch.from_numpy(host).to(dev),
+                      "emb": torch.from_numpy(e).to(dev)})
+        refs.append(oracle.run_video(host, e))
+    res = ctx.run_videos(items, want_cos=True)
+    for n, r, ref in zip(ns, res, refs):
+        assert list(r.detected) == list(ref.detected)
+        assert list(r.final) == list(ref.final)
+        assert r.n_candidates == ref.n_candidates
+    last = (1000 - 1) // 8 * 8
+    want = list(range(8, last + 1, 8))
+    if 1000 - want[-1] < 8:
+        want = want[:-1]
+    assert list(res[0].detected) == want
