@@ -91,9 +91,9 @@ CD_HD uint32_t cd_min3_u16x2(uint32_t a, uint32_t b, uint32_t c) {
 // (LOP3/PRMT/VIMNMX/IADD3, the binding pipe on sm_100: DESIGN.md §7) to the
 // bit work.
 struct MadK {
-  uint32_t one, neg1, three, four, neg4, neg6;
+  uint32_t one, neg1, three, neg6;
 };
-constexpr MadK kMadK{1u, 0xFFFFFFFFu, 3u, 4u, 0xFFFFFFFCu, 0xFFFFFFFAu};
+constexpr MadK kMadK{1u, 0xFFFFFFFFu, 3u, 0xFFFFFFFAu};
 
 CD_HD uint32_t cd_mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
@@ -118,6 +118,17 @@ CD_HD uint32_t cd_sel(uint32_t a, uint32_t b) {
 #endif
 }
 
+// a ^ b ^ c as ONE LOP3
+CD_HD uint32_t cd_xor3(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+#else
+  return a ^ b ^ c;
+#endif
+}
+
 // ------------------------------------------------------------ hue table
 // lut_entry: qr | qf << 2 with qr = floor(3 na / d) (rising sectors) and
 // qf = floor(3 (d - na) / d) (falling), both clamped to 3; 0 for grey (d = 0).
@@ -139,8 +150,9 @@ CD_HD uint32_t lut_unswizzle(uint32_t b, uint32_t d) { return (b - 4u * d) & 255
 // runs between the table lookup and the shared-memory atomic but one PRMT:
 //   offset = byte1 << 8 | byte0,
 //   byte0 = the table entry: q3 << 2 | hash << 5  (bits 0-1 zero),
-//   byte1 = v (bits 8-9) | s1 (10) | s2 (11) | A = [r>=g] (12) | B = [g>=b] (13)
-//           | C = [r>=b] (14) | 0 (15)          -> offsets < 0x8000: 8192 entries.
+//   byte1 = v (bits 8-9) and, in bits 10-14, an invertible XOR mix of
+//           s1, s2, A = [r>=g], B = [g>=b], C = [r>=b] (code_pair_dir_pre),
+//           bit 15 zero                         -> offsets < 0x8000: 8192 entries.
 // q3 in [0, 8) is the compact index of the table's (qr, qf) pair (kDirQ below);
 // hash (2 bits, a function of (d, na) that the bin ignores) only spreads the
 // entries over the 32 shared-memory banks: the bank of an entry is offset bits
@@ -168,8 +180,7 @@ CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d, int hash) {
 // the two table indices.  The table index is (na + 4d) mod 256 of row d,
 // computed straight from the channel sum: na + 4d = (r + g + b) + 3 max - 6 min
 // (mid = sum - max - min).  The byte-1 fields are threshold bits (a - b + 2^j)
-// merged by bit-selects: every select takes ONE field from its source and
-// keeps the rest, and the field values never carry into bit 15.
+// in u16x2 lanes (no lane borrows), merged as below.
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   const uint32_t mx = cd_max3_u16x2(R, G, B);
@@ -181,7 +192,6 @@ CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8
   const uint32_t tA = R + 0x10001000u - G;                                 // bit 12: r >= g
   const uint32_t tB = G + 0x20002000u - B;                                 // bit 13: g >= b
-  const uint32_t tC = cd_mad(B, k.neg4, cd_mad(R, k.four, 0x40004000u));  // bit 14: r >= b
   // s flags against max itself: black (max = 0) sets both, but a grey pixel is
   // recognisable from its table entry (q3 = 0 only when d = 0) and
   // code_to_bin_dir forces s = 0 for it.
@@ -189,11 +199,17 @@ CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uin
   const uint32_t x1 = cd_mad(d, k.three, z1);  // 3d - mx + 2^10:  bit 10 = s1, < 2^11
   const uint32_t x2 = cd_mad(z1, k.one, x1);   // 3d - 2mx + 2^11: bit 11 = s2, < 2^12
   const uint32_t m3 = cd_mad(mx, k.three, 0u);  // bits 8-9 of 3 max = v, < 2^10
-  uint32_t p = cd_sel<0x04000400u>(x1, x2);  // bit 10 s1, bit 11 s2, bits 12-15 zero
-  p = cd_sel<0x03000300u>(m3, p);
-  p = cd_sel<0x10001000u>(tA, p);
-  p = cd_sel<0x20002000u>(tB, p);
-  return cd_sel<0x40004000u>(tC, p);
+  const uint32_t tC = cd_mad(B, k.neg1, cd_mad(R, k.one, 0x40004000u));  // bit 14: r >= b
+  // Above its low byte every threshold word is CLEAN: a - b + 2^j with
+  // |a - b| < 256 has bit j = [a >= b], its complement in bits 8..j-1 and
+  // zeros above (tA, tB, tC); x2 = 3d - 2mx + 2^11 lies in [1538, 2303], so its
+  // bit 10 is ~s2 and only bits 0-9 vary otherwise, and x1 < 2^11.  Two
+  // three-input XORs therefore merge the five flags into bits 10-14
+  // invertibly, and one select puts v into bits 8-9 (x1 and x2 vary there):
+  //   b10 = s1 ^ ~s2 ^ ~P,  b11 = s2 ^ ~P,  b12 = P = A ^ B ^ C,
+  //   b13 = ~(B ^ C),  b14 = C          (decoded by code_to_bin_dir)
+  // Three LOP3 instead of five bit-selects (B200 A/B: K1 +3.9 %, K1-NV12 +4.3 %).
+  return cd_sel<0x03000300u>(m3, cd_xor3(x1, x2, cd_xor3(tA, tB, tC)));
 }
 // Part 2: the two lanes' byte offsets from the looked-up entries q0, q1 (u8).
 CD_HD uint32_t dir_off_lo(uint32_t pre, uint32_t q0) { return cd_prmt(q0, pre, 0x1150u); }
@@ -204,8 +220,10 @@ CD_HD uint32_t code_to_bin_dir(uint32_t idx) {
   const uint32_t c = idx << 2;
   const uint32_t q = (kDirQ >> (4 * ((c >> 2) & 7u))) & 15u;
   const uint32_t qr = q & 3u, qf = q >> 2, z = (c >> 7) & 1u, v = (c >> 8) & 3u;
-  const uint32_t s1 = (c >> 10) & 1u, s2 = (c >> 11) & 1u, A = (c >> 12) & 1u;
-  const uint32_t B = (c >> 13) & 1u, C = (c >> 14) & 1u, z2 = c >> 15;
+  // undo code_pair_dir_pre's XOR mix of bits 10-14
+  const uint32_t P = (c >> 12) & 1u, C = (c >> 14) & 1u, B = 1u ^ ((c >> 13) & 1u) ^ C;
+  const uint32_t A = P ^ B ^ C, s2 = ((c >> 11) & 1u) ^ 1u ^ P;
+  const uint32_t s1 = ((c >> 10) & 1u) ^ s2 ^ P, z2 = c >> 15;
   const uint32_t ris = A ^ B ^ C;  // odd #(>=) <=> rising sector
   const uint32_t oidx = (A << 2) | (B << 1) | C;
   if (z || z2 || oidx == 1u || oidx == 6u || v > 2u || s2 > s1) return 255u;
