@@ -181,12 +181,17 @@ CD_HD uint32_t lut_entry_dir(uint32_t na, uint32_t d, int hash) {
 // computed straight from the channel sum: na + 4d = (r + g + b) + 3 max - 6 min
 // (mid = sum - max - min).  The byte-1 fields are threshold bits (a - b + 2^j)
 // in u16x2 lanes (no lane borrows), merged as below.
+// SUM_ALU: r + g + b by one IADD3 (ALU pipe) instead of two IMADs (FMA pipe):
+// one issue slot less, one ALU instruction more — K1 gains (+3.1 %, its ALU pipe
+// has room), K1-NV12 loses (−1.0 %, its conversion already loads the ALU pipe).
+template <bool SUM_ALU = false>
 CD_HD uint32_t code_pair_dir_pre(uint32_t R, uint32_t G, uint32_t B, MadK k, uint32_t& i0,
                                  uint32_t& i1) {
   const uint32_t mx = cd_max3_u16x2(R, G, B);
   const uint32_t mn = cd_min3_u16x2(R, G, B);
   const uint32_t d = cd_mad(mn, k.neg1, mx);
-  const uint32_t t = cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, k.three, R)));
+  const uint32_t t = SUM_ALU ? cd_mad(mx, k.three, R + G + B)
+                             : cd_mad(B, k.one, cd_mad(G, k.one, cd_mad(mx, k.three, R)));
   const uint32_t nas = cd_mad(mn, k.neg6, t);  // na + 4d; lanes < 2^16
   i0 = cd_prmt(nas, d, 0x5540u);  // lane 0: nas.b0 | d.b0 << 8
   i1 = cd_prmt(nas, d, 0x7762u);  // lane 1: nas.b2 | d.b2 << 8

@@ -157,8 +157,8 @@ __device__ __forceinline__ void bin_quads(const uint8_t* buf, int q0, int qstrid
   for (int j = 0; j < NQ; ++j) {
     uint32_t R01, G01, B01, R23, G23, B23;
     unpack4(w[j][0], w[j][1], w[j][2], R01, G01, B01, R23, G23, B23);
-    pre[2 * j] = code_pair_dir_pre(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
-    pre[2 * j + 1] = code_pair_dir_pre(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
+    pre[2 * j] = code_pair_dir_pre<true>(R01, G01, B01, mk, ia[2 * j], ib[2 * j]);
+    pre[2 * j + 1] = code_pair_dir_pre<true>(R23, G23, B23, mk, ia[2 * j + 1], ib[2 * j + 1]);
   }
   uint32_t qa[2 * NQ], qb[2 * NQ];
 #pragma unroll
@@ -435,7 +435,7 @@ k5_binmap_kernel(uint8_t* __restrict__ out, uint32_t nh, uint32_t ns, uint32_t n
     const uint32_t R = r | ((c2 >> 16) << 16), G = g | (((c2 >> 8) & 255u) << 16),
                    B = b | ((c2 & 255u) << 16);
     uint32_t i0, i1;
-    const uint32_t pre = code_pair_dir_pre(R, G, B, mk, i0, i1);
+    const uint32_t pre = code_pair_dir_pre<true>(R, G, B, mk, i0, i1);
     out[c] = (uint8_t)code_to_bin_dir(dir_off_lo(pre, lut[i0]) >> 2);                // lane 0
     out[(1u << 24) + c2] = (uint8_t)code_to_bin_dir(dir_off_hi(pre, lut[i1]) >> 2);  // lane 1
   }

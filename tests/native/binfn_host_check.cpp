@@ -42,7 +42,7 @@ int main(int argc, char** argv) {
     const uint32_t B = (c & 255u) | ((c2 & 255u) << 16);
     tg[c] = (uint8_t)bin_generic(c >> 16, (c >> 8) & 255u, c & 255u, nh, ns, nv);
     uint32_t i0, i1;
-    const uint32_t dp = code_pair_dir_pre(R, G, B, kMadK, i0, i1);
+    const uint32_t dp = code_pair_dir_pre<true>(R, G, B, kMadK, i0, i1);
     const uint32_t o0 = dir_off_lo(dp, lut_rgb[i0]), o1 = dir_off_hi(dp, lut_rgb[i1]);
     if (o0 >= 4u * kDirCodes || o1 >= 4u * kDirCodes || (o0 & 3u) || (o1 & 3u)) {
       fprintf(stderr, "dir code offset out of range\n");
